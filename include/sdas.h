@@ -1,0 +1,236 @@
+/* include/sdas.h -- C-ABI of the B200-native SDAS strategy simulator.
+ *
+ * What it computes: a batched Monte-Carlo discrete-event simulation of agent
+ * pipelines (e.g. developer -> tester, Fig. 1) whose inter-agent
+ * message granularity is batching / function-by-function pipelining /
+ * token-level streaming, optionally switched per window by a
+ * metrics-driven controller, swept over
+ * candidates x request rates x profiles x seeds, with exact per-replica
+ * p50/p99 end-to-end and first-feedback latency, throughput, queue-length
+ * series and an argmin over candidates.  The model rules M0-M20 are stated in
+ * DESIGN.md §"Model" (SURVEY.md §8(c) readings).
+ *
+ * Conventions (all entry points):
+ *  - Every quantity is an integer; 1 tick = 1 microsecond (rule M0).
+ *  - Status codes are returned, never thrown; sdas_last_error() holds a
+ *    thread-local message naming the offending field (valid until the next
+ *    sdas_* call on the same thread).
+ *  - The library NEVER allocates device memory.  The caller (PyTorch in the
+ *    Python binding) allocates every buffer named in sdas_buffers with the byte
+ *    sizes returned by sdas_results_layout(), 256-byte aligned.
+ *  - Launches are asynchronous on `stream` (a cudaStream_t passed as void*).
+ *  - Descriptors are deep-copied by sdas_pipeline_create; grid pointers are read
+ *    only during the call.
+ */
+#ifndef SDAS_H
+#define SDAS_H
+#include <stddef.h>
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int32_t sdas_status;
+#define SDAS_OK 0
+#define SDAS_E_INVALID_ARG -1   /* null pointer, bad enum, zero-length axis */
+#define SDAS_E_INVALID_FIELD -2 /* descriptor invariant violated (SPEC.md:53 InvalidField); message names it */
+#define SDAS_E_UNKNOWN_PARAM -3 /* set/reset on an unregistered knob (Table 1) */
+#define SDAS_E_OUT_OF_RANGE -4  /* set value outside the knob's range (e.g. max_num_seqs 0) */
+#define SDAS_E_BUFFER -5        /* a required buffer is NULL or misaligned */
+#define SDAS_E_CUDA -6          /* CUDA launch / runtime error; message carries cudaGetErrorString */
+#define SDAS_E_STATE -7         /* call order violated (e.g. sdas_metrics GROUP scope before control_sweep) */
+#define SDAS_E_LIMIT -8         /* exceeds an implementation limit (shared-memory budget, instance count) */
+
+const char* sdas_last_error(void);
+const char* sdas_version(void);
+
+/* ---- enums ---------------------------------------------------------------------- */
+enum { SDAS_BATCH = 0, SDAS_FUNCTION = 1, SDAS_TOKEN = 2 };            /* PAPER.md:17 (a)(b)(c) */
+enum { SDAS_ROUTE_JSQ = 0, SDAS_ROUTE_RR = 1, SDAS_ROUTE_FIXED = 2, SDAS_ROUTE_SELECT = 3,
+       SDAS_ROUTE_NONE = 255 };
+enum { SDAS_SVC_DET = 0, SDAS_SVC_EXP = 1 };
+enum { SDAS_POISSON = 0, SDAS_MMPP2 = 1, SDAS_DET = 2, SDAS_LIST = 3 };  /* PAPER.md:38 "varying load" */
+enum { SDAS_STATIC = 0, SDAS_ADAPTIVE = 1 };
+enum { SDAS_METRIC_BUSY = 0, SDAS_METRIC_LOAD = 1 };
+enum { SDAS_REPLICA_OK = 0, SDAS_REPLICA_OVERFLOW = 1, SDAS_REPLICA_TRUNCATED = 2 };
+enum { SDAS_MIN_P99_E2E = 0, SDAS_MIN_P50_E2E = 1, SDAS_MIN_P99_FF = 2, SDAS_MAX_THROUGHPUT = 3,
+       SDAS_MAX_GOODPUT = 4, SDAS_MAX_LARGE_FRAC_UNDER_SLO = 5 };          /* rule M20 */
+enum { SDAS_SCOPE_REPLICA = 0, SDAS_SCOPE_CELL = 1, SDAS_SCOPE_GROUP = 2, SDAS_SCOPE_ROW = 3 };
+
+#define SDAS_FLAG_RECORDS 1u /* write per-request (e2e, ff) records to buffers.records */
+#define SDAS_FLAG_SERIES 2u  /* write per-window queue-length series for sampled replicas */
+#define SDAS_FLAG_TRACE 4u   /* write the event trace of grid.trace_replica (debug) */
+
+/* implementation limits (DESIGN.md §"Limits") */
+#define SDAS_MAX_ROLES 8
+#define SDAS_MAX_INSTANCES 8
+#define SDAS_MAX_LINKS 7
+#define SDAS_MAX_OUT 2       /* out-links per role (fan-out) */
+#define SDAS_MAX_BATCH 32    /* max_num_seqs upper bound: one lane per sequence */
+#define SDAS_MAX_REQUESTS 65535
+#define SDAS_NBINS 464       /* rule M17: log-linear bins over u32 latencies */
+#define SDAS_NCNT 24         /* int64 counters per cell */
+#define SDAS_SUMMARY_BYTES 128
+
+/* ---- pipeline description ---------- */
+typedef struct {           /* per-message and per-token service model of one agent instance */
+  uint32_t h_msg;          /* receive overhead per message (SPEC.md:203 h_rx, charged at the receiver) */
+  uint32_t alpha, beta;    /* RECV(m) = h_msg + beta*m.tokens + alpha*[m opens an item]  (rule M7) */
+  uint32_t tau0, gamma;    /* DECODE step = tau0 + gamma*b for batch size b            (rule M7) */
+  uint32_t large;          /* 1 = LARGE model profile (model selection) */
+} sdas_cost;
+
+typedef struct {
+  uint32_t n_instances;       /* 1..SDAS_MAX_INSTANCES in total over all roles */
+  sdas_cost cost;             /* default cost of every instance */
+  const sdas_cost* inst_cost; /* NULL, or [n_instances] per-instance overrides (copied) */
+  uint32_t max_num_seqs;      /* default B, 1..32; knob "agent:<role>/max_num_seqs" */
+  uint32_t out_fixed, out_num, out_den; /* non-source item output = out_fixed + n_in*out_num/out_den (M8) */
+  uint32_t n_functions;       /* F: FUNCTION segments of this role's outputs (M8) */
+  uint32_t svc;               /* SDAS_SVC_DET | SDAS_SVC_EXP (alpha ~ Exp(mean alpha) per item) */
+  uint32_t route;             /* routing INTO this role when n_instances > 1 (M11) */
+  uint32_t route_fixed;       /* instance for SDAS_ROUTE_FIXED */
+  uint32_t inbox_cap;         /* delivered-not-started messages per instance (M14) */
+  uint32_t flight_cap;        /* emitted-not-delivered messages addressed to an instance (M14) */
+  uint32_t wait_cap;          /* items waiting for batch admission per instance (M14) */
+} sdas_role_desc;
+
+typedef struct {
+  uint32_t src_role, dst_role; /* src < dst (DAG in topological order); role 0 is the only source */
+  uint32_t net_delay;          /* >= 1 tick; delivery = emit + net_delay */
+  uint32_t chunk_tokens;       /* >= 1; TOKEN(c) chunk; knob "link:<s>-><d>/chunk_tokens" */
+  uint32_t mode;               /* default granularity; knob "link:<s>-><d>/comm_mode" */
+} sdas_link_desc;
+
+typedef struct {
+  uint32_t n_roles; const sdas_role_desc* roles;   /* role 0 = the source */
+  uint32_t n_links; const sdas_link_desc* links;   /* every non-source role has exactly one in-link */
+  uint32_t feedback_role;                           /* first-feedback is measured here (M13) */
+  uint32_t request_cap;                             /* R_cap: admitted-not-completed requests (M14) */
+  uint64_t window_ticks;                            /* metrics/control window W (M15), 1..2^31-1 */
+  uint64_t slo_ticks;                               /* "good" completions: e2e <= slo (M19) */
+} sdas_pipeline_desc;
+
+typedef struct sdas_pipeline sdas_pipeline;
+
+/* Deep-copies and validates `desc`.  Errors: SDAS_E_INVALID_ARG (NULL), SDAS_E_INVALID_FIELD
+ * (message names the field), SDAS_E_LIMIT.  On success *out owns a pipeline (sdas_pipeline_destroy). */
+sdas_status sdas_pipeline_create(const sdas_pipeline_desc* desc, sdas_pipeline** out);
+void sdas_pipeline_destroy(sdas_pipeline* p); /* NULL-safe */
+
+/* Table 1: set(parameter, value) / reset(parameter) on the pipeline's
+ * knob registry ("each agent exposes ... knobs").  Knobs (SPEC.md:209, 498 addressing):
+ *   "agent:<role>/max_num_seqs"      1..32      (default: desc value)
+ *   "agent:<role>/n_functions"       1..65535
+ *   "link:<src>-><dst>/comm_mode"    0..2       (SDAS_BATCH/FUNCTION/TOKEN)
+ *   "link:<src>-><dst>/chunk_tokens" 1..65535
+ *   "link:<src>-><dst>/net_delay"    1..2^31-1
+ * Values set here are the initial knob values of every replica; reset restores the value given
+ * at sdas_pipeline_create (idempotent).  Errors: SDAS_E_UNKNOWN_PARAM, SDAS_E_OUT_OF_RANGE. */
+sdas_status sdas_set(sdas_pipeline* p, const char* knob, int64_t value);
+sdas_status sdas_reset(sdas_pipeline* p, const char* knob);
+sdas_status sdas_get(const sdas_pipeline* p, const char* knob, int64_t* value);
+
+/* ---- sweep grid ------------------------------------------------------------------- */
+typedef struct {
+  uint32_t kind;              /* STATIC | ADAPTIVE workload policy (M16) */
+  uint8_t mode[8];            /* per link: static mode / adaptive initial mode; 255 = pipeline knob */
+  uint32_t ctl_links;         /* ADAPTIVE: bitmask of links whose comm_mode the controller drives */
+  uint32_t metric;            /* SDAS_METRIC_BUSY | SDAS_METRIC_LOAD of the link's destination role */
+  uint32_t lo_permille, hi_permille, dwell_windows; /* three-band thresholds and dwell D (M16(i)) */
+  uint8_t band_mode[4];       /* modes for the low / mid / high band ([3] unused) */
+  uint32_t route_override;    /* SDAS_ROUTE_NONE, or JSQ/RR for every JSQ/RR role (M11) */
+  uint32_t batch_roles;       /* bitmask of roles with SLO-aware max_num_seqs control (M16(ii)) */
+  uint32_t q_hi;              /* M16(ii): grow B when the window's integral Q > q_hi * W */
+  int32_t select_role;        /* -1, or the SELECT role driven by model selection (M16(iii)) */
+  uint64_t policy_slo_ticks;  /* SLO used by the controller's window p99 test */
+} sdas_candidate;
+
+typedef struct {
+  uint32_t kind;              /* SDAS_POISSON | MMPP2 | DET | LIST */
+  uint64_t mean_gap[2];       /* ticks; [1] = high-rate state of MMPP2; gap*2977044472 < 2^64 */
+  uint64_t mean_sojourn[2];   /* MMPP2 epoch means (low, high) */
+  const uint64_t* list;       /* LIST: nondecreasing arrival ticks, list_len >= n_requests */
+  uint32_t list_len;
+  uint32_t prompt_lo, prompt_hi, out_lo, out_hi; /* P ~ U[lo,hi], O ~ U[lo,hi] (M5), <= 65535 */
+} sdas_arrival_desc;
+
+typedef struct {
+  uint32_t n_candidates; const sdas_candidate* cand;          /* axis c */
+  uint32_t n_rates, n_profiles; const sdas_arrival_desc* arrivals; /* [n_rates * n_profiles], axes i, k */
+  uint32_t n_seeds, seed_offset; uint64_t master_seed;         /* axis s; Philox key (M2) */
+  uint32_t n_requests;                                         /* N per replica, 1..65535 */
+  uint64_t max_ticks;                                          /* 0 = none; else TRUNCATED beyond */
+  uint32_t flags;                                              /* SDAS_FLAG_* */
+  uint32_t series_stride, series_slots, series_windows;        /* replicas r = m*stride, m < slots */
+  uint64_t group_begin, group_end;   /* global group range [begin, end) of this call; end 0 = all */
+  uint32_t rank, world;              /* group-interleaved partition: group g runs on rank g % world */
+  uint64_t trace_replica; uint32_t trace_cap;                  /* SDAS_FLAG_TRACE */
+} sdas_grid;
+/* Replica id r = g*C + c with group g = (i*K + k)*S + s (rule M1).  The replicas of this call are
+ * the groups g in [group_begin, group_end) with g % world == rank, all C candidates of each; local
+ * replica x = lg*C + c for the lg-th such group. */
+
+typedef struct {
+  uint64_t params_bytes;     /* device: packed descriptors (written by the library) */
+  uint64_t work_bytes;       /* device: scratch (replica counter + per-warp record scratch) */
+  uint64_t summary_bytes;    /* device: n_local_replicas x 128-byte summary records */
+  uint64_t records_bytes;    /* device: n_local_replicas x n_requests x {u32 e2e, u32 ff} (FLAG_RECORDS) */
+  uint64_t series_bytes;     /* device: series_slots x series_windows x n_instances x 16 B (FLAG_SERIES) */
+  uint64_t cell_cnt_bytes;   /* device: n_cells x SDAS_NCNT int64 (zeroed by the caller; accumulated) */
+  uint64_t cell_hist_bytes;  /* device: n_cells x 2 x SDAS_NBINS int32 (zeroed by the caller) */
+  uint64_t best_group_bytes; /* device: n_local_groups int32 (control_sweep) */
+  uint64_t best_row_bytes;   /* device: n_rows int32 (finalize) */
+  uint64_t trace_bytes;      /* device: 8 + trace_cap x 24 B (FLAG_TRACE) */
+  uint64_t n_local_replicas, n_local_groups, n_groups, n_cells, n_rows, n_replicas;
+  uint32_t n_instances, smem_per_replica, warps_per_block, blocks_per_sm;
+  uint64_t resident_replicas;
+} sdas_layout;
+
+typedef struct {
+  void *params, *work, *summary, *records, *series, *cell_cnt, *cell_hist, *best_group, *best_row, *trace;
+} sdas_buffers;
+
+/* Sizes of every buffer for (p, grid) on the current device (queries the occupancy). */
+sdas_status sdas_results_layout(const sdas_pipeline* p, const sdas_grid* grid, sdas_layout* out);
+
+/* Simulate every local replica (K1, one replica per warp) and merge its histograms and counters
+ * into the cell buffers (integer atomics).  Writes summaries (+ records / series / trace per
+ * flags).  Required buffers: params, work, summary, cell_cnt, cell_hist.  Asynchronous. */
+sdas_status sdas_simulate(const sdas_pipeline* p, const sdas_grid* grid, const sdas_buffers* dev, void* stream);
+
+/* sdas_simulate + the per-group argmin over candidates (K3) for `objective` (rule M20).
+ * Also requires best_group.  objective_slo is the SLO of SDAS_MAX_LARGE_FRAC_UNDER_SLO. */
+sdas_status sdas_control_sweep(const sdas_pipeline* p, const sdas_grid* grid, uint32_t objective,
+                               uint64_t objective_slo, const sdas_buffers* dev, void* stream);
+
+/* Per-row (i, k) argmin over pooled cells (after the caller's all_reduce of the cell buffers). */
+sdas_status sdas_finalize(const sdas_pipeline* p, const sdas_grid* grid, uint32_t objective,
+                          uint64_t objective_slo, const sdas_buffers* dev, void* stream);
+
+/* ---- metrics queries on HOST copies of the buffers (PAPER.md:231-238 metrics plane) ---- */
+typedef struct {
+  uint32_t status;
+  uint64_t n_replicas, admitted, dropped, completed;
+  uint32_t p50_e2e, p99_e2e, p50_ff, p99_ff;      /* exact (REPLICA) or bin lower edge (CELL/ROW) */
+  uint32_t bin_p50_e2e, bin_p99_e2e, bin_p50_ff, bin_p99_ff;
+  double mean_e2e, mean_ff;                       /* (double)sum / (double)n  (M19) */
+  double throughput, goodput;                     /* completed*1e6/makespan, good*1e6/makespan (req/s) */
+  uint64_t makespan, sum_e2e, sum_ff, int_nsys, good, large_items;
+  uint64_t arrivals, deliveries, recv_steps, decode_steps, window_closes, mode_switches, tokens;
+  uint64_t message_events, des_events;            /* arrivals + deliveries; + steps + window closes */
+  int32_t best;                                   /* GROUP / ROW scope: winning candidate */
+  const uint8_t* series;                          /* REPLICA scope with FLAG_SERIES: 16 B records */
+  uint64_t series_len;                            /* windows x instances */
+} sdas_metrics_out;
+
+/* host: host copies of the device buffers (only those the scope needs, same layout).
+ * REPLICA: index = local replica; CELL: index = cell (i*K + k)*C + c; GROUP: local group;
+ * ROW: index = (i*K + k).  Errors: SDAS_E_INVALID_ARG, SDAS_E_STATE (missing buffer). */
+sdas_status sdas_metrics(const sdas_pipeline* p, const sdas_grid* grid, const sdas_buffers* host,
+                         uint32_t scope, uint64_t index, sdas_metrics_out* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SDAS_H */

@@ -336,13 +336,14 @@ struct Replica {
     uint64_t ffl = ff[j] - A[j];
     uint32_t e32 = e2e > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)e2e;
     uint32_t f32 = ffl > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)ffl;
-    if (e2e > 0xFFFFFFFFull || ffl > 0xFFFFFFFFull) S.n_saturated++;
+    // saturated iff a field reaches 2^32-1 (reading R-SAT); sum_ff sums saturated values
+    if (e2e >= 0xFFFFFFFFull || ffl >= 0xFFFFFFFFull) S.n_saturated++;
     if (rec) { rec[2 * S.completed] = e32; rec[2 * S.completed + 1] = f32; }
     hist[bin_of(e32)]++;
     hist[ORC_NBINS + bin_of(f32)]++;
     S.completed++;
     S.sum_e2e += e2e;
-    S.sum_ff += ffl;
+    S.sum_ff += f32;
     S.max_e2e = std::max(S.max_e2e, e32);
     if (e2e <= P.slo) S.good++;
     w_n++;

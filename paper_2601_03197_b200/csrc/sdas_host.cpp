@@ -1,0 +1,650 @@
+// sdas_host.cpp -- host side of libsdas: the C-ABI of include/sdas.h.
+//
+// Validation (SPEC.md:53 InvalidField conventions), the Table-1 knob registry (PAPER.md:196-217:
+// set/reset, "each agent exposes ... knobs"), grid partitioning (group-interleaved over ranks,
+// DESIGN.md §"Multi-GPU"), shared-memory layout planning for K1, packing of the device parameter
+// block, launches on the caller's stream, and metric queries on host copies.
+// No device memory is allocated here: the caller (PyTorch) owns every buffer.
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "sdas_internal.h"
+
+using namespace sdas;
+
+namespace {
+
+thread_local std::string g_err;
+
+sdas_status fail(sdas_status code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+sdas_status ok() {
+  g_err.clear();
+  return SDAS_OK;
+}
+
+// Q32 log2 table T[i] = round(2^32 log2(1 + i/256)) (rule M3), evaluated here through log1p.
+struct Log2Tab {
+  uint64_t t[257];
+  Log2Tab() {
+    const long double inv_ln2 = 1.0L / logl(2.0L);
+    for (int i = 0; i <= 256; ++i) t[i] = (uint64_t)llroundl(ldexpl(log1pl((long double)i / 256.0L) * inv_ln2, 32));
+  }
+};
+const Log2Tab& log2tab() {
+  static Log2Tab T;
+  return T;
+}
+
+uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
+
+}  // namespace
+
+struct sdas_pipeline {
+  std::vector<sdas_role_desc> roles;
+  std::vector<std::vector<sdas_cost>> inst_cost;
+  std::vector<sdas_link_desc> links;
+  uint32_t feedback_role = 0, request_cap = 0;
+  uint64_t window = 0, slo = 0;
+  // knob registry: current values and registered defaults (Table 1)
+  std::vector<uint32_t> B_cur, B_def, F_cur, F_def;
+  std::vector<uint32_t> mode_cur, mode_def, chunk_cur, chunk_def, net_cur, net_def;
+  uint32_t n_inst = 0;
+};
+
+namespace {
+
+sdas_status validate_desc(const sdas_pipeline_desc* d) {
+  if (!d) return fail(SDAS_E_INVALID_ARG, "desc is NULL");
+  if (d->n_roles == 0 || !d->roles) return fail(SDAS_E_INVALID_FIELD, "n_roles: at least one role required");
+  if (d->n_roles > SDAS_MAX_ROLES) return fail(SDAS_E_LIMIT, "n_roles: at most %d", SDAS_MAX_ROLES);
+  if (d->n_links > SDAS_MAX_LINKS) return fail(SDAS_E_LIMIT, "n_links: at most %d", SDAS_MAX_LINKS);
+  if (d->n_links && !d->links) return fail(SDAS_E_INVALID_FIELD, "links: NULL with n_links > 0");
+  if (d->feedback_role >= d->n_roles) return fail(SDAS_E_INVALID_FIELD, "feedback_role: out of range");
+  if (d->request_cap < 1 || d->request_cap > 4096)
+    return fail(SDAS_E_INVALID_FIELD, "request_cap: must be in 1..4096");
+  if (d->window_ticks < 1 || d->window_ticks >= (1ull << 31))
+    return fail(SDAS_E_INVALID_FIELD, "window_ticks: must be in 1..2^31-1");
+  uint32_t n_inst = 0;
+  for (uint32_t r = 0; r < d->n_roles; ++r) {
+    const sdas_role_desc& R = d->roles[r];
+    if (R.n_instances < 1) return fail(SDAS_E_INVALID_FIELD, "roles[%u].n_instances: must be >= 1", r);
+    n_inst += R.n_instances;
+    if (R.max_num_seqs < 1 || R.max_num_seqs > SDAS_MAX_BATCH)
+      return fail(SDAS_E_INVALID_FIELD, "roles[%u].max_num_seqs: must be in 1..32", r);
+    if (R.out_den < 1) return fail(SDAS_E_INVALID_FIELD, "roles[%u].out_den: must be >= 1", r);
+    if (R.n_functions < 1 || R.n_functions > 65535)
+      return fail(SDAS_E_INVALID_FIELD, "roles[%u].n_functions: must be in 1..65535", r);
+    if (R.svc > SDAS_SVC_EXP) return fail(SDAS_E_INVALID_FIELD, "roles[%u].svc: bad enum", r);
+    if (R.route > SDAS_ROUTE_SELECT) return fail(SDAS_E_INVALID_FIELD, "roles[%u].route: bad enum", r);
+    if (R.route == SDAS_ROUTE_FIXED && R.route_fixed >= R.n_instances)
+      return fail(SDAS_E_INVALID_FIELD, "roles[%u].route_fixed: out of range", r);
+    if (R.inbox_cap < 1 || R.inbox_cap > 65535 || R.wait_cap < 1 || R.wait_cap > 65535 || R.flight_cap > 65535 ||
+        (r > 0 && R.flight_cap < 1))
+      return fail(SDAS_E_INVALID_FIELD, "roles[%u].caps: inbox/wait in 1..65535, flight in 1..65535", r);
+    const sdas_cost* cs = R.inst_cost;
+    for (uint32_t x = 0; x < R.n_instances; ++x) {
+      const sdas_cost& c = cs ? cs[x] : R.cost;
+      if (c.h_msg >= (1u << 31) || c.alpha >= (1u << 31) || c.beta >= (1u << 15) || c.tau0 >= (1u << 31) ||
+          c.gamma >= (1u << 25))
+        return fail(SDAS_E_INVALID_FIELD, "roles[%u].cost: step costs must stay below 2^31 ticks", r);
+    }
+  }
+  if (n_inst > SDAS_MAX_INSTANCES) return fail(SDAS_E_LIMIT, "instances: at most %d in total", SDAS_MAX_INSTANCES);
+  std::vector<int> indeg(d->n_roles, 0), outdeg(d->n_roles, 0);
+  for (uint32_t l = 0; l < d->n_links; ++l) {
+    const sdas_link_desc& L = d->links[l];
+    if (L.dst_role >= d->n_roles || L.src_role >= L.dst_role)
+      return fail(SDAS_E_INVALID_FIELD, "links[%u]: need src_role < dst_role < n_roles", l);
+    if (L.net_delay < 1 || L.net_delay >= (1u << 31))
+      return fail(SDAS_E_INVALID_FIELD, "links[%u].net_delay: must be in 1..2^31-1", l);
+    if (L.chunk_tokens < 1 || L.chunk_tokens > 65535)
+      return fail(SDAS_E_INVALID_FIELD, "links[%u].chunk_tokens: must be in 1..65535", l);
+    if (L.mode > SDAS_TOKEN) return fail(SDAS_E_INVALID_FIELD, "links[%u].mode: bad enum", l);
+    indeg[L.dst_role]++;
+    outdeg[L.src_role]++;
+  }
+  for (uint32_t r = 1; r < d->n_roles; ++r)
+    if (indeg[r] != 1) return fail(SDAS_E_INVALID_FIELD, "roles[%u]: needs exactly one in-link (role 0 is the only source, no joins)", r);
+  for (uint32_t r = 0; r < d->n_roles; ++r)
+    if (outdeg[r] > SDAS_MAX_OUT) return fail(SDAS_E_LIMIT, "roles[%u]: at most %d out-links", r, SDAS_MAX_OUT);
+  return SDAS_OK;
+}
+
+int parse_knob(const sdas_pipeline* p, const char* knob, int* kind, uint32_t* idx) {
+  // returns 0 ok; kinds: 0 max_num_seqs, 1 n_functions, 2 comm_mode, 3 chunk_tokens, 4 net_delay
+  if (!knob) return -1;
+  unsigned a = 0, b = 0;
+  char name[64] = {0};
+  int n = 0;
+  if (sscanf(knob, "agent:%u/%63s%n", &a, name, &n) == 2 && knob[n] == 0) {
+    if (a >= p->roles.size()) return -1;
+    *idx = a;
+    if (!strcmp(name, "max_num_seqs")) { *kind = 0; return 0; }
+    if (!strcmp(name, "n_functions")) { *kind = 1; return 0; }
+    return -1;
+  }
+  n = 0;
+  if (sscanf(knob, "link:%u->%u/%63s%n", &a, &b, name, &n) == 3 && knob[n] == 0) {
+    for (uint32_t l = 0; l < p->links.size(); ++l) {
+      if (p->links[l].src_role == a && p->links[l].dst_role == b) {
+        *idx = l;
+        if (!strcmp(name, "comm_mode")) { *kind = 2; return 0; }
+        if (!strcmp(name, "chunk_tokens")) { *kind = 3; return 0; }
+        if (!strcmp(name, "net_delay")) { *kind = 4; return 0; }
+        return -1;
+      }
+    }
+  }
+  return -1;
+}
+
+struct Plan {
+  DParams hp;
+  uint64_t n_groups = 0, n_cells = 0, n_rows = 0, n_replicas = 0;
+  uint32_t wpb = 1, blocks_per_sm = 1, n_sm = 148, smem_block = 0, blocks = 0;
+  uint64_t total_warps = 0;
+  uint64_t blob_bytes = 0;
+};
+
+sdas_status plan(const sdas_pipeline* p, const sdas_grid* g, Plan& pl) {
+  if (!p || !g) return fail(SDAS_E_INVALID_ARG, "pipeline or grid is NULL");
+  if (g->n_candidates == 0 || !g->cand) return fail(SDAS_E_INVALID_ARG, "grid.n_candidates: must be >= 1");
+  if (g->n_rates == 0 || g->n_profiles == 0 || !g->arrivals)
+    return fail(SDAS_E_INVALID_ARG, "grid.n_rates/n_profiles: must be >= 1");
+  if (g->n_seeds == 0) return fail(SDAS_E_INVALID_ARG, "grid.n_seeds: must be >= 1");
+  if (g->n_requests < 1 || g->n_requests > SDAS_MAX_REQUESTS)
+    return fail(SDAS_E_INVALID_FIELD, "grid.n_requests: must be in 1..65535");
+  if (g->world < 1 || g->rank >= g->world) return fail(SDAS_E_INVALID_ARG, "grid.rank/world: need rank < world");
+  const uint32_t nl = (uint32_t)p->links.size();
+  for (uint32_t c = 0; c < g->n_candidates; ++c) {
+    const sdas_candidate& cd = g->cand[c];
+    if (cd.kind > SDAS_ADAPTIVE) return fail(SDAS_E_INVALID_FIELD, "cand[%u].kind: bad enum", c);
+    for (uint32_t l = 0; l < nl; ++l)
+      if (cd.mode[l] != 255 && cd.mode[l] > SDAS_TOKEN) return fail(SDAS_E_INVALID_FIELD, "cand[%u].mode[%u]", c, l);
+    for (int b = 0; b < 3; ++b)
+      if (cd.band_mode[b] > SDAS_TOKEN) return fail(SDAS_E_INVALID_FIELD, "cand[%u].band_mode[%d]", c, b);
+    if (cd.ctl_links >> nl) return fail(SDAS_E_INVALID_FIELD, "cand[%u].ctl_links: unknown link", c);
+    if (cd.batch_roles >> p->roles.size()) return fail(SDAS_E_INVALID_FIELD, "cand[%u].batch_roles", c);
+    if (cd.select_role >= (int32_t)p->roles.size()) return fail(SDAS_E_INVALID_FIELD, "cand[%u].select_role", c);
+    if (cd.route_override != SDAS_ROUTE_NONE && cd.route_override > SDAS_ROUTE_RR)
+      return fail(SDAS_E_INVALID_FIELD, "cand[%u].route_override: NONE, JSQ or RR", c);
+    if (cd.metric > SDAS_METRIC_LOAD || cd.lo_permille > 1000000 || cd.hi_permille > 1000000 || cd.dwell_windows > (1u << 30))
+      return fail(SDAS_E_INVALID_FIELD, "cand[%u]: metric/lo/hi/dwell out of range", c);
+  }
+  const uint64_t nIK = (uint64_t)g->n_rates * g->n_profiles;
+  for (uint64_t a = 0; a < nIK; ++a) {
+    const sdas_arrival_desc& A = g->arrivals[a];
+    if (A.kind > SDAS_LIST) return fail(SDAS_E_INVALID_FIELD, "arrivals[%llu].kind: bad enum", (unsigned long long)a);
+    if (A.prompt_lo > A.prompt_hi || A.prompt_hi > 65535 || A.out_lo > A.out_hi || A.out_hi > 65535)
+      return fail(SDAS_E_INVALID_FIELD, "arrivals[%llu]: prompt/out ranges must be lo <= hi <= 65535",
+                  (unsigned long long)a);
+    const uint64_t lim = UINT64_MAX / 2977044472ull;
+    if (A.kind == SDAS_POISSON || A.kind == SDAS_MMPP2) {
+      for (int z = 0; z < (A.kind == SDAS_MMPP2 ? 2 : 1); ++z) {
+        if (A.mean_gap[z] >= lim || A.mean_gap[z] > (1ull << 35))
+          return fail(SDAS_E_INVALID_FIELD, "arrivals[%llu].mean_gap: too large", (unsigned long long)a);
+        if (A.kind == SDAS_MMPP2 && A.mean_sojourn[z] >= lim)
+          return fail(SDAS_E_INVALID_FIELD, "arrivals[%llu].mean_sojourn: too large", (unsigned long long)a);
+      }
+    }
+    if (A.kind == SDAS_LIST) {
+      if (!A.list || A.list_len < g->n_requests)
+        return fail(SDAS_E_INVALID_FIELD, "arrivals[%llu].list: need list_len >= n_requests", (unsigned long long)a);
+      for (uint32_t j = 1; j < g->n_requests; ++j)
+        if (A.list[j] < A.list[j - 1])
+          return fail(SDAS_E_INVALID_FIELD, "arrivals[%llu].list: must be nondecreasing", (unsigned long long)a);
+    }
+  }
+  // requests per slot index must fit u16 slots; request_cap <= 4096 validated
+  DParams& h = pl.hp;
+  memset(&h, 0, sizeof(h));
+  h.n_roles = (uint32_t)p->roles.size();
+  h.n_links = nl;
+  h.n_inst = p->n_inst;
+  h.feedback_role = p->feedback_role;
+  h.request_cap = p->request_cap;
+  h.n_requests = g->n_requests;
+  h.flags = g->flags;
+  h.bitmap_words = (p->request_cap + 31) / 32;
+  h.C = g->n_candidates; h.I = g->n_rates; h.K = g->n_profiles; h.S = g->n_seeds;
+  h.seed_offset = g->seed_offset; h.rank = g->rank; h.world = g->world;
+  h.series_stride = g->series_stride; h.series_slots = g->series_slots; h.series_windows = g->series_windows;
+  h.trace_cap = g->trace_cap;
+  h.window = p->window; h.slo = p->slo; h.max_ticks = g->max_ticks; h.master_seed = g->master_seed;
+  h.trace_replica = g->trace_replica;
+  pl.n_groups = nIK * g->n_seeds;
+  pl.n_rows = nIK;
+  pl.n_cells = nIK * g->n_candidates;
+  pl.n_replicas = pl.n_groups * g->n_candidates;
+  const uint64_t gb = g->group_begin, ge = g->group_end ? std::min<uint64_t>(g->group_end, pl.n_groups) : pl.n_groups;
+  if (gb > ge) return fail(SDAS_E_INVALID_ARG, "grid.group_begin > group_end");
+  const uint64_t first = gb + (uint64_t)((g->rank + g->world - (gb % g->world)) % g->world);
+  h.first_group = first;
+  h.n_local_groups = first < ge ? (ge - first + g->world - 1) / g->world : 0;
+  h.n_local_replicas = h.n_local_groups * g->n_candidates;
+
+  // --- topology
+  uint32_t inst = 0;
+  for (uint32_t r = 0; r < h.n_roles; ++r) {
+    const sdas_role_desc& R = p->roles[r];
+    DRole& D = h.role[r];
+    D.first = inst; D.n = R.n_instances; D.route = R.route; D.route_fixed = R.route_fixed;
+    D.out_fixed = R.out_fixed; D.out_num = R.out_num; D.out_den = R.out_den; D.n_functions = p->F_cur[r];
+    D.in_link = -1;
+    D.large_inst = inst;
+    D.small_inst = inst + R.n_instances - 1;
+    for (uint32_t x = R.n_instances; x-- > 0;) if (p->inst_cost[r][x].large) D.large_inst = inst + x;
+    for (uint32_t x = R.n_instances; x-- > 0;) if (!p->inst_cost[r][x].large) D.small_inst = inst + x;
+    for (uint32_t x = 0; x < R.n_instances; ++x) {
+      DInst& I = h.inst[inst + x];
+      const sdas_cost& c = p->inst_cost[r][x];
+      I.role = r; I.h = c.h_msg; I.alpha = c.alpha; I.beta = c.beta; I.tau0 = c.tau0; I.gamma = c.gamma;
+      I.B_default = p->B_cur[r];
+      I.flags = (c.large ? 1u : 0u) | (R.svc == SDAS_SVC_EXP ? 2u : 0u);
+      I.inbox_cap = R.inbox_cap; I.flight_cap = r > 0 ? R.flight_cap : 0; I.wait_cap = R.wait_cap;
+    }
+    inst += R.n_instances;
+  }
+  for (uint32_t l = 0; l < nl; ++l) {
+    const sdas_link_desc& L = p->links[l];
+    DLink& D = h.link[l];
+    D.src = L.src_role; D.dst = L.dst_role; D.net = p->net_cur[l]; D.chunk = p->chunk_cur[l]; D.mode = p->mode_cur[l];
+    DRole& S = h.role[L.src_role];
+    if (S.n_out == 0) S.out_link0 = l; else S.out_link1 = l;
+    S.n_out++;
+    h.role[L.dst_role].in_link = (int32_t)l;
+  }
+  for (uint32_t r = 0; r < h.n_roles; ++r) h.role[r].batch_words = 2 + 2 * h.role[r].n_out;
+
+  // --- shared-memory layout of one warp's replica
+  uint64_t o = 256;  // WarpHdr
+  const uint32_t R = p->request_cap;
+  h.off_reqA = (uint32_t)o; o += 8ull * R;
+  h.off_reqFF = (uint32_t)o; o += 4ull * R;
+  h.off_reqJ = (uint32_t)o; o += 4ull * R;
+  h.off_reqO = (uint32_t)o; o += 2ull * R;
+  h.off_reqNit = (uint32_t)o; o += 2ull * R;
+  h.off_reqOut = (uint32_t)o; o += 2ull * R;
+  o = align_up(o, 16);
+  h.off_bitmap = (uint32_t)o; o += 4ull * h.bitmap_words;
+  for (uint32_t i = 0; i < h.n_inst; ++i) {
+    DInst& I = h.inst[i];
+    o = align_up(o, 16);
+    I.off_inbox = (uint32_t)o; o += 8ull * I.inbox_cap;
+    o = align_up(o, 16);
+    I.off_ftick = (uint32_t)o; o += 4ull * I.flight_cap;
+    o = align_up(o, 16);
+    I.off_fbody = (uint32_t)o; o += 8ull * I.flight_cap;
+    o = align_up(o, 16);
+    I.off_wait = (uint32_t)o; o += 4ull * I.wait_cap;
+    o = align_up(o, 16);
+    I.off_batch = (uint32_t)o; o += 4ull * 32 * h.role[I.role].batch_words;
+  }
+  o = align_up(o, 16);
+  h.off_scratch = 256;
+  const uint64_t need = std::max<uint64_t>(o, 256 + (uint64_t)kScratchMin);
+  h.smem_per_warp = (uint32_t)align_up(need, 16);
+  h.off_warps = (uint32_t)align_up(sizeof(DParams), 128);
+
+  // --- occupancy: choose warps per block maximizing resident warps per SM
+  const uint64_t smem_cap = 227 * 1024;
+  if (h.off_warps + h.smem_per_warp > smem_cap)
+    return fail(SDAS_E_LIMIT, "replica needs %u B of shared memory (max %llu): reduce caps or request_cap",
+                h.smem_per_warp, (unsigned long long)(smem_cap - h.off_warps));
+  int n_sm = 148;
+  uint32_t best_w = 1, best_b = 1;
+  uint64_t best_tot = 0;
+  bool have_dev = false;
+  for (uint32_t wpb = 1; wpb <= 8; ++wpb) {
+    const uint64_t sb = h.off_warps + (uint64_t)wpb * h.smem_per_warp;
+    if (sb > smem_cap) break;
+    int bps = 0, nsm = 0;
+    if (query_occupancy(wpb, (uint32_t)sb, &bps, &nsm) == 0 && bps > 0) {
+      have_dev = true;
+      n_sm = nsm;
+    } else {
+      bps = (int)std::min<uint64_t>(32, (228 * 1024) / (sb + 1024));
+      bps = std::min(bps, (int)(64 / wpb));
+    }
+    const uint64_t tot = (uint64_t)bps * wpb;
+    if (tot >= best_tot) { best_tot = tot; best_w = wpb; best_b = (uint32_t)bps; }
+  }
+  (void)have_dev;
+  pl.wpb = best_w;
+  pl.blocks_per_sm = best_b;
+  pl.n_sm = (uint32_t)n_sm;
+  pl.smem_block = (uint32_t)(h.off_warps + (uint64_t)best_w * h.smem_per_warp);
+  const uint64_t want_blocks = (h.n_local_replicas + best_w - 1) / best_w;
+  pl.blocks = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)n_sm * best_b, want_blocks));
+  pl.total_warps = (uint64_t)pl.blocks * best_w;
+
+  // --- blob: DParams | candidates | arrivals | LIST ticks
+  uint64_t b = align_up(sizeof(DParams), 64);
+  h.off_cand = b; b += 64ull * g->n_candidates;
+  h.off_arr = b; b += 64ull * nIK;
+  for (uint64_t a = 0; a < nIK; ++a)
+    if (g->arrivals[a].kind == SDAS_LIST) b += 8ull * g->n_requests;
+  pl.blob_bytes = align_up(b, 256);
+  return SDAS_OK;
+}
+
+void pack_blob(const sdas_grid* g, const Plan& pl, std::vector<uint8_t>& blob) {
+  blob.assign(pl.blob_bytes, 0);
+  memcpy(blob.data(), &pl.hp, sizeof(DParams));
+  DCand* dc = reinterpret_cast<DCand*>(blob.data() + pl.hp.off_cand);
+  for (uint32_t c = 0; c < g->n_candidates; ++c) {
+    const sdas_candidate& s = g->cand[c];
+    DCand& d = dc[c];
+    d.adaptive = s.kind == SDAS_ADAPTIVE;
+    for (int l = 0; l < 8; ++l) d.mode[l] = s.mode[l];
+    d.ctl_links = s.ctl_links; d.metric_load = s.metric == SDAS_METRIC_LOAD;
+    d.lo = s.lo_permille; d.hi = s.hi_permille; d.dwell = s.dwell_windows;
+    for (int k = 0; k < 4; ++k) d.band[k] = s.band_mode[k];
+    d.route_override = s.route_override; d.batch_roles = s.batch_roles; d.q_hi = s.q_hi;
+    d.select_role = s.select_role; d.policy_slo = s.policy_slo_ticks;
+  }
+  const uint64_t nIK = (uint64_t)g->n_rates * g->n_profiles;
+  DArr* da = reinterpret_cast<DArr*>(blob.data() + pl.hp.off_arr);
+  uint64_t lo = pl.hp.off_arr + 64ull * nIK;
+  for (uint64_t a = 0; a < nIK; ++a) {
+    const sdas_arrival_desc& s = g->arrivals[a];
+    DArr& d = da[a];
+    d.kind = s.kind; d.list_len = s.list_len;
+    d.gap0 = s.mean_gap[0]; d.gap1 = s.mean_gap[1]; d.soj0 = s.mean_sojourn[0]; d.soj1 = s.mean_sojourn[1];
+    d.p_lo = s.prompt_lo; d.p_hi = s.prompt_hi; d.o_lo = s.out_lo; d.o_hi = s.out_hi;
+    if (s.kind == SDAS_LIST) {
+      d.list_off = lo;
+      memcpy(blob.data() + lo, s.list, 8ull * g->n_requests);
+      lo += 8ull * g->n_requests;
+    }
+  }
+}
+
+sdas_status fill_layout(const Plan& pl, const sdas_grid* g, sdas_layout* L) {
+  memset(L, 0, sizeof(*L));
+  const DParams& h = pl.hp;
+  L->params_bytes = pl.blob_bytes;
+  const uint64_t scratch = pl.total_warps * (uint64_t)g->n_requests * 8ull;
+  L->work_bytes = align_up(sizeof(Work) + std::max<uint64_t>(scratch, pl.n_cells * 4ull), 256);
+  L->summary_bytes = align_up(std::max<uint64_t>(1, h.n_local_replicas) * SDAS_SUMMARY_BYTES, 256);
+  L->records_bytes = (g->flags & SDAS_FLAG_RECORDS) ? align_up(h.n_local_replicas * g->n_requests * 8ull, 256) : 0;
+  L->series_bytes = (g->flags & SDAS_FLAG_SERIES)
+                        ? align_up((uint64_t)g->series_slots * g->series_windows * h.n_inst * 16ull, 256) : 0;
+  L->cell_cnt_bytes = align_up(pl.n_cells * SDAS_NCNT * 8ull, 256);
+  L->cell_hist_bytes = align_up(pl.n_cells * 2ull * SDAS_NBINS * 4ull, 256);
+  L->best_group_bytes = align_up(std::max<uint64_t>(1, h.n_local_groups) * 4ull, 256);
+  L->best_row_bytes = align_up(std::max<uint64_t>(1, pl.n_rows) * 4ull, 256);
+  L->trace_bytes = (g->flags & SDAS_FLAG_TRACE) ? align_up(8ull + 24ull * g->trace_cap, 256) : 0;
+  L->n_local_replicas = h.n_local_replicas;
+  L->n_local_groups = h.n_local_groups;
+  L->n_groups = pl.n_groups;
+  L->n_cells = pl.n_cells;
+  L->n_rows = pl.n_rows;
+  L->n_replicas = pl.n_replicas;
+  L->n_instances = h.n_inst;
+  L->smem_per_replica = h.smem_per_warp;
+  L->warps_per_block = pl.wpb;
+  L->blocks_per_sm = pl.blocks_per_sm;
+  L->resident_replicas = pl.total_warps;
+  return SDAS_OK;
+}
+
+bool aligned(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 255u) == 0; }
+
+}  // namespace
+
+extern "C" {
+
+const char* sdas_last_error(void) { return g_err.c_str(); }
+const char* sdas_version(void) { return "sdas-b200 0.1 (sm_100a)"; }
+
+sdas_status sdas_pipeline_create(const sdas_pipeline_desc* desc, sdas_pipeline** out) {
+  if (!out) return fail(SDAS_E_INVALID_ARG, "out is NULL");
+  *out = nullptr;
+  sdas_status s = validate_desc(desc);
+  if (s != SDAS_OK) return s;
+  sdas_pipeline* p = new sdas_pipeline();
+  p->roles.assign(desc->roles, desc->roles + desc->n_roles);
+  p->links.assign(desc->links, desc->links + desc->n_links);
+  p->inst_cost.resize(desc->n_roles);
+  for (uint32_t r = 0; r < desc->n_roles; ++r) {
+    const sdas_role_desc& R = desc->roles[r];
+    for (uint32_t x = 0; x < R.n_instances; ++x) p->inst_cost[r].push_back(R.inst_cost ? R.inst_cost[x] : R.cost);
+    p->roles[r].inst_cost = nullptr;  // deep-copied above
+    p->B_def.push_back(R.max_num_seqs);
+    p->F_def.push_back(R.n_functions);
+    p->n_inst += R.n_instances;
+  }
+  for (const sdas_link_desc& L : p->links) {
+    p->mode_def.push_back(L.mode);
+    p->chunk_def.push_back(L.chunk_tokens);
+    p->net_def.push_back(L.net_delay);
+  }
+  p->B_cur = p->B_def; p->F_cur = p->F_def;
+  p->mode_cur = p->mode_def; p->chunk_cur = p->chunk_def; p->net_cur = p->net_def;
+  p->feedback_role = desc->feedback_role;
+  p->request_cap = desc->request_cap;
+  p->window = desc->window_ticks;
+  p->slo = desc->slo_ticks;
+  *out = p;
+  return ok();
+}
+
+void sdas_pipeline_destroy(sdas_pipeline* p) { delete p; }
+
+sdas_status sdas_set(sdas_pipeline* p, const char* knob, int64_t value) {
+  if (!p || !knob) return fail(SDAS_E_INVALID_ARG, "pipeline or knob is NULL");
+  int kind;
+  uint32_t idx;
+  if (parse_knob(p, knob, &kind, &idx)) return fail(SDAS_E_UNKNOWN_PARAM, "unknown parameter '%s'", knob);
+  static const int64_t lo[5] = {1, 1, 0, 1, 1};
+  static const int64_t hi[5] = {SDAS_MAX_BATCH, 65535, SDAS_TOKEN, 65535, (1ll << 31) - 1};
+  if (value < lo[kind] || value > hi[kind])
+    return fail(SDAS_E_OUT_OF_RANGE, "value %lld out of range [%lld, %lld] for '%s'", (long long)value,
+                (long long)lo[kind], (long long)hi[kind], knob);
+  std::vector<uint32_t>* v[5] = {&p->B_cur, &p->F_cur, &p->mode_cur, &p->chunk_cur, &p->net_cur};
+  (*v[kind])[idx] = (uint32_t)value;
+  return ok();
+}
+
+sdas_status sdas_reset(sdas_pipeline* p, const char* knob) {
+  if (!p || !knob) return fail(SDAS_E_INVALID_ARG, "pipeline or knob is NULL");
+  int kind;
+  uint32_t idx;
+  if (parse_knob(p, knob, &kind, &idx)) return fail(SDAS_E_UNKNOWN_PARAM, "unknown parameter '%s'", knob);
+  std::vector<uint32_t>* cur[5] = {&p->B_cur, &p->F_cur, &p->mode_cur, &p->chunk_cur, &p->net_cur};
+  std::vector<uint32_t>* def[5] = {&p->B_def, &p->F_def, &p->mode_def, &p->chunk_def, &p->net_def};
+  (*cur[kind])[idx] = (*def[kind])[idx];
+  return ok();
+}
+
+sdas_status sdas_get(const sdas_pipeline* p, const char* knob, int64_t* value) {
+  if (!p || !knob || !value) return fail(SDAS_E_INVALID_ARG, "NULL argument");
+  int kind;
+  uint32_t idx;
+  if (parse_knob(p, knob, &kind, &idx)) return fail(SDAS_E_UNKNOWN_PARAM, "unknown parameter '%s'", knob);
+  const std::vector<uint32_t>* cur[5] = {&p->B_cur, &p->F_cur, &p->mode_cur, &p->chunk_cur, &p->net_cur};
+  *value = (*cur[kind])[idx];
+  return ok();
+}
+
+sdas_status sdas_results_layout(const sdas_pipeline* p, const sdas_grid* grid, sdas_layout* out) {
+  if (!out) return fail(SDAS_E_INVALID_ARG, "out is NULL");
+  Plan pl;
+  sdas_status s = plan(p, grid, pl);
+  if (s != SDAS_OK) return s;
+  fill_layout(pl, grid, out);
+  return ok();
+}
+
+static sdas_status run_sim(const sdas_pipeline* p, const sdas_grid* g, const sdas_buffers* d, void* stream,
+                           Plan& pl) {
+  if (!d) return fail(SDAS_E_INVALID_ARG, "buffers is NULL");
+  sdas_status s = plan(p, g, pl);
+  if (s != SDAS_OK) return s;
+  if (!d->params || !d->work || !d->summary || !d->cell_cnt || !d->cell_hist)
+    return fail(SDAS_E_BUFFER, "params, work, summary, cell_cnt and cell_hist are required");
+  if (!aligned(d->params) || !aligned(d->work) || !aligned(d->summary) || !aligned(d->cell_cnt) ||
+      !aligned(d->cell_hist))
+    return fail(SDAS_E_BUFFER, "device buffers must be 256-byte aligned");
+  if ((g->flags & SDAS_FLAG_RECORDS) && !d->records) return fail(SDAS_E_BUFFER, "FLAG_RECORDS needs records");
+  if ((g->flags & SDAS_FLAG_SERIES) && !d->series) return fail(SDAS_E_BUFFER, "FLAG_SERIES needs series");
+  if ((g->flags & SDAS_FLAG_TRACE) && !d->trace) return fail(SDAS_E_BUFFER, "FLAG_TRACE needs trace");
+  std::vector<uint8_t> blob;
+  pack_blob(g, pl, blob);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  cudaError_t e = cudaMemcpyAsync(d->params, blob.data(), blob.size(), cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) return fail(SDAS_E_CUDA, "params upload: %s", cudaGetErrorString(e));
+  int rc = launch_simulate(reinterpret_cast<const uint8_t*>(d->params), pl.hp, d, pl.blocks, pl.wpb, pl.smem_block,
+                           stream, log2tab().t);
+  if (rc) return fail(SDAS_E_CUDA, "K1 launch: %s", cuda_error_string(rc));
+  // the pageable-memory async copy has been staged when cudaMemcpyAsync returned; `blob` may go
+  return SDAS_OK;
+}
+
+sdas_status sdas_simulate(const sdas_pipeline* p, const sdas_grid* grid, const sdas_buffers* dev, void* stream) {
+  Plan pl;
+  sdas_status s = run_sim(p, grid, dev, stream, pl);
+  return s == SDAS_OK ? ok() : s;
+}
+
+sdas_status sdas_control_sweep(const sdas_pipeline* p, const sdas_grid* grid, uint32_t objective,
+                               uint64_t objective_slo, const sdas_buffers* dev, void* stream) {
+  if (objective > SDAS_MAX_LARGE_FRAC_UNDER_SLO) return fail(SDAS_E_INVALID_ARG, "objective: bad enum");
+  if (dev && !dev->best_group) return fail(SDAS_E_BUFFER, "control_sweep needs best_group");
+  Plan pl;
+  sdas_status s = run_sim(p, grid, dev, stream, pl);
+  if (s != SDAS_OK) return s;
+  int rc = launch_group_argmin(reinterpret_cast<const uint8_t*>(dev->params), pl.hp, dev, objective, objective_slo,
+                               stream);
+  if (rc) return fail(SDAS_E_CUDA, "K3 launch: %s", cuda_error_string(rc));
+  return ok();
+}
+
+sdas_status sdas_finalize(const sdas_pipeline* p, const sdas_grid* grid, uint32_t objective, uint64_t objective_slo,
+                          const sdas_buffers* dev, void* stream) {
+  if (objective > SDAS_MAX_LARGE_FRAC_UNDER_SLO) return fail(SDAS_E_INVALID_ARG, "objective: bad enum");
+  if (!dev || !dev->params || !dev->work || !dev->cell_cnt || !dev->cell_hist || !dev->best_row)
+    return fail(SDAS_E_BUFFER, "finalize needs params, work, cell_cnt, cell_hist and best_row");
+  Plan pl;
+  sdas_status s = plan(p, grid, pl);
+  if (s != SDAS_OK) return s;
+  std::vector<uint8_t> blob;
+  pack_blob(grid, pl, blob);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  cudaError_t e = cudaMemcpyAsync(dev->params, blob.data(), sizeof(DParams), cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) return fail(SDAS_E_CUDA, "params upload: %s", cudaGetErrorString(e));
+  int rc = launch_finalize(reinterpret_cast<const uint8_t*>(dev->params), pl.hp, dev, objective, objective_slo,
+                           pl.n_cells, pl.n_rows, stream);
+  if (rc) return fail(SDAS_E_CUDA, "K4/K5 launch: %s", cuda_error_string(rc));
+  return ok();
+}
+
+sdas_status sdas_metrics(const sdas_pipeline* p, const sdas_grid* grid, const sdas_buffers* host, uint32_t scope,
+                         uint64_t index, sdas_metrics_out* out) {
+  if (!p || !grid || !host || !out) return fail(SDAS_E_INVALID_ARG, "NULL argument");
+  Plan pl;
+  sdas_status s = plan(p, grid, pl);
+  if (s != SDAS_OK) return s;
+  memset(out, 0, sizeof(*out));
+  out->best = -1;
+  auto derive = [&]() {  // M19 fp64 derived values from integer sums
+    out->mean_e2e = out->completed ? (double)out->sum_e2e / (double)out->completed : 0.0;
+    out->mean_ff = out->completed ? (double)out->sum_ff / (double)out->completed : 0.0;
+    out->throughput = out->makespan ? (double)(out->completed * 1000000ull) / (double)out->makespan : 0.0;
+    out->goodput = out->makespan ? (double)(out->good * 1000000ull) / (double)out->makespan : 0.0;
+    out->message_events = out->arrivals + out->deliveries;
+    out->des_events = out->message_events + out->recv_steps + out->decode_steps + out->window_closes;
+  };
+  if (scope == SDAS_SCOPE_REPLICA) {
+    if (!host->summary) return fail(SDAS_E_STATE, "REPLICA scope needs summary");
+    if (index >= pl.hp.n_local_replicas) return fail(SDAS_E_INVALID_ARG, "index out of range");
+    const uint32_t* w = reinterpret_cast<const uint32_t*>(reinterpret_cast<const uint8_t*>(host->summary) +
+                                                          index * SDAS_SUMMARY_BYTES);
+    auto u64 = [&](int k) { return (uint64_t)w[k] | ((uint64_t)w[k + 1] << 32); };
+    out->status = w[0]; out->n_replicas = 1; out->admitted = w[1]; out->dropped = w[2]; out->completed = w[3];
+    out->makespan = u64(4); out->sum_e2e = u64(6); out->sum_ff = u64(8); out->int_nsys = u64(10);
+    out->p50_e2e = w[12]; out->p99_e2e = w[13]; out->p50_ff = w[14]; out->p99_ff = w[15];
+    out->bin_p50_e2e = w[16] & 0xFFFF; out->bin_p99_e2e = w[16] >> 16;
+    out->bin_p50_ff = w[17] & 0xFFFF; out->bin_p99_ff = w[17] >> 16;
+    out->arrivals = w[20]; out->deliveries = w[21]; out->recv_steps = w[22]; out->decode_steps = w[23];
+    out->window_closes = w[24]; out->mode_switches = w[25]; out->good = w[26]; out->large_items = w[27];
+    out->tokens = u64(28);
+    derive();
+    if (host->series && (grid->flags & SDAS_FLAG_SERIES) && grid->series_stride) {
+      const uint64_t lg = index / pl.hp.C, c = index % pl.hp.C;
+      const uint64_t rid = (pl.hp.first_group + lg * pl.hp.world) * pl.hp.C + c;
+      if (rid % grid->series_stride == 0 && rid / grid->series_stride < grid->series_slots) {
+        const uint64_t per = (uint64_t)grid->series_windows * pl.hp.n_inst;
+        out->series = reinterpret_cast<const uint8_t*>(host->series) + (rid / grid->series_stride) * per * 16;
+        out->series_len = std::min<uint64_t>(per, (uint64_t)(w[24] + 1) * pl.hp.n_inst);
+      }
+    }
+    return ok();
+  }
+  if (scope == SDAS_SCOPE_CELL) {
+    if (!host->cell_cnt || !host->cell_hist) return fail(SDAS_E_STATE, "CELL scope needs cell_cnt and cell_hist");
+    if (index >= pl.n_cells) return fail(SDAS_E_INVALID_ARG, "index out of range");
+    const int64_t* q = reinterpret_cast<const int64_t*>(host->cell_cnt) + index * SDAS_NCNT;
+    const int32_t* h = reinterpret_cast<const int32_t*>(host->cell_hist) + index * 2 * SDAS_NBINS;
+    out->status = q[1] == q[0] ? SDAS_REPLICA_OK : SDAS_REPLICA_OVERFLOW;
+    out->n_replicas = q[0]; out->admitted = q[4]; out->dropped = q[5]; out->completed = q[6];
+    out->sum_e2e = q[7]; out->sum_ff = q[8]; out->makespan = q[9]; out->int_nsys = q[10]; out->good = q[11];
+    out->large_items = q[12]; out->arrivals = q[13]; out->deliveries = q[14]; out->recv_steps = q[15];
+    out->decode_steps = q[16]; out->window_closes = q[17]; out->mode_switches = q[18]; out->tokens = q[19];
+    auto pct = [&](const int32_t* hh, uint32_t num, uint32_t* val, uint32_t* bin) {
+      uint64_t n = 0;
+      for (int b = 0; b < SDAS_NBINS; ++b) n += (uint32_t)hh[b];
+      *val = 0xFFFFFFFFu;
+      *bin = 0xFFFFu;
+      if (!n) return;
+      const uint64_t k = (num * n + 99) / 100;
+      uint64_t cum = 0;
+      for (uint32_t b = 0; b < SDAS_NBINS; ++b) {
+        cum += (uint32_t)hh[b];
+        if (cum >= k) {
+          *bin = b;
+          *val = b < 16 ? b : (16u + ((b - 16u) & 15u)) << ((b - 16u) >> 4);
+          return;
+        }
+      }
+    };
+    pct(h, 50, &out->p50_e2e, &out->bin_p50_e2e);
+    pct(h, 99, &out->p99_e2e, &out->bin_p99_e2e);
+    pct(h + SDAS_NBINS, 50, &out->p50_ff, &out->bin_p50_ff);
+    pct(h + SDAS_NBINS, 99, &out->p99_ff, &out->bin_p99_ff);
+    derive();
+    return ok();
+  }
+  if (scope == SDAS_SCOPE_GROUP) {
+    if (!host->best_group) return fail(SDAS_E_STATE, "GROUP scope needs best_group (run sdas_control_sweep)");
+    if (index >= pl.hp.n_local_groups) return fail(SDAS_E_INVALID_ARG, "index out of range");
+    out->best = reinterpret_cast<const int32_t*>(host->best_group)[index];
+    return ok();
+  }
+  if (scope == SDAS_SCOPE_ROW) {
+    if (!host->best_row) return fail(SDAS_E_STATE, "ROW scope needs best_row (run sdas_finalize)");
+    if (index >= pl.n_rows) return fail(SDAS_E_INVALID_ARG, "index out of range");
+    out->best = reinterpret_cast<const int32_t*>(host->best_row)[index];
+    return ok();
+  }
+  return fail(SDAS_E_INVALID_ARG, "scope: bad enum");
+}
+
+}  // extern "C"

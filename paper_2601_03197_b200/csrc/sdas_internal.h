@@ -1,0 +1,90 @@
+// Internal device-side parameter block of libsdas (product path only; not shared with oracle/).
+// The host library packs a DParams header followed by candidates, arrival descriptors and LIST
+// tick arrays into the caller-provided `params` device buffer; K1 copies DParams into shared
+// memory once per CTA.
+#pragma once
+#include <stdint.h>
+
+#include "../../include/sdas.h"
+
+namespace sdas {
+
+constexpr uint32_t kUnsetFF = 0xFFFFFFFFu;   // ff latency not yet observed (also "saturated")
+constexpr uint32_t kNever = 0xFFFFFFFFu;
+constexpr int kScratchMin = 2 * SDAS_NBINS * 4 + 256 * 4 + 128 + SDAS_NCNT * 8;  // finalize scratch
+
+struct DInst {          // one instance, 64 B
+  uint32_t role, h, alpha, beta, tau0, gamma, B_default, flags;   // flags: bit0 large, bit1 svc_exp
+  uint32_t inbox_cap, flight_cap, wait_cap;
+  uint32_t off_inbox, off_ftick, off_fbody, off_wait, off_batch;  // byte offsets inside the warp region
+};
+
+struct DRole {          // one role, 64 B
+  uint32_t first, n, route, route_fixed;
+  uint32_t out_fixed, out_num, out_den, n_functions;
+  int32_t in_link;
+  uint32_t n_out, out_link0, out_link1;
+  uint32_t large_inst, small_inst, batch_words, pad;      // batch_words = 2 + 2*n_out per slot
+};
+
+struct DLink {          // one link, 32 B
+  uint32_t src, dst, net, chunk, mode, pad0, pad1, pad2;
+};
+
+struct DCand {          // one candidate, 64 B
+  uint32_t adaptive;
+  uint8_t mode[8];
+  uint32_t ctl_links, metric_load, lo, hi, dwell;
+  uint8_t band[4];
+  uint32_t route_override, batch_roles, q_hi;
+  int32_t select_role;
+  uint64_t policy_slo;
+};
+
+struct DArr {           // one arrival descriptor, 64 B
+  uint32_t kind, list_len;
+  uint64_t gap0, gap1, soj0, soj1;
+  uint64_t list_off;    // byte offset of the LIST ticks inside the params blob
+  uint32_t p_lo, p_hi, o_lo, o_hi;
+};
+
+struct alignas(16) DParams {
+  uint32_t n_roles, n_links, n_inst, feedback_role;
+  uint32_t request_cap, n_requests, flags, bitmap_words;
+  uint32_t C, I, K, S;
+  uint32_t seed_offset, rank, world, series_stride;
+  uint32_t series_slots, series_windows, trace_cap, smem_per_warp;
+  uint32_t off_warps;        // byte offset of warp 0's region in the CTA's shared memory
+  uint32_t off_reqA, off_reqFF, off_reqJ, off_reqO, off_reqNit, off_reqOut, off_bitmap, off_scratch;
+  uint32_t pad0;
+  uint64_t window, slo, max_ticks, master_seed;
+  uint64_t first_group, n_local_groups, n_local_replicas, trace_replica;
+  uint64_t off_cand, off_arr;
+  DInst inst[SDAS_MAX_INSTANCES];
+  DRole role[SDAS_MAX_ROLES];
+  DLink link[SDAS_MAX_LINKS + 1];
+};
+
+static_assert(sizeof(DInst) == 64, "DInst");
+static_assert(sizeof(DRole) == 64, "DRole");
+static_assert(sizeof(DCand) == 64, "DCand");
+static_assert(sizeof(DArr) == 64, "DArr");
+static_assert(sizeof(DParams) % 16 == 0, "DParams");
+
+struct Work {              // head of the `work` buffer
+  unsigned long long next_replica;
+  unsigned long long pad[31];
+  // followed by per-warp record scratch: total_warps x n_requests x u64
+};
+
+// Launch wrappers implemented in sdas_kernels.cu (host-callable).
+int launch_simulate(const uint8_t* params_dev, const DParams& hp, const sdas_buffers* b, uint32_t blocks,
+                    uint32_t warps_per_block, uint32_t smem_bytes, void* stream, const uint64_t* log2_table);
+int launch_group_argmin(const uint8_t* params_dev, const DParams& hp, const sdas_buffers* b, uint32_t objective,
+                        uint64_t slo, void* stream);
+int launch_finalize(const uint8_t* params_dev, const DParams& hp, const sdas_buffers* b, uint32_t objective,
+                    uint64_t slo, uint64_t n_cells, uint64_t n_rows, void* stream);
+int query_occupancy(uint32_t warps_per_block, uint32_t smem_bytes, int* blocks_per_sm, int* n_sm);
+const char* cuda_error_string(int code);
+
+}  // namespace sdas

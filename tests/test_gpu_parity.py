@@ -1,0 +1,135 @@
+"""GPU (libsdas sm_100a, through the C-ABI) vs CPU oracle parity.
+
+Bar (BASELINE.json north_star): histograms, event counts, percentiles and controller decisions
+bit-exact (time is integer); derived fp64 means to 1e-12 relative.  Sizes here span several
+waves of the persistent kernel and ragged tails; test_gpu_fullsize.py covers the bench
+configuration at full size on sampled replicas.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import workloads as W
+from gpu_parity import compare_records, compare_summaries, first_divergence, full_check, run_gpu, sorted_trace
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("mode", ["token", "function", "batch"])
+def test_ht0_spec_trace(mode):
+    p = W.p2_spec(mode=mode, chunk=16, n_functions=2)
+    g = W.grid([W.static(mode)], [W.arr_list([0], prompt=(100, 100), output=(32, 32))], n_requests=1)
+    gg, o = full_check(p, g)
+    assert int(gg["summary"][0]["p50_e2e"]) == {"token": 780800, "function": 657800, "batch": 786600}[mode]
+
+
+@pytest.mark.parametrize("mode", ["batch", "function", "token"])
+def test_ht13(mode):
+    p = W.toy_ht(mode)
+    g = W.grid([W.static(mode)], [W.arr_list([0, 3])], n_requests=2, series_stride=1, series_slots=1,
+               series_windows=1)
+    full_check(p, g, series=True)
+
+
+@pytest.mark.parametrize("mode", ["batch", "function", "token"])
+def test_trace_equivalence(mode):
+    p = W.p2_x(mode=mode)
+    g = W.grid([W.static(mode)], [W.poisson(570571)], n_seeds=2, n_requests=150)
+    gg = run_gpu(p, g, trace_replica=1)
+    o = oracle.simulate(p, g, trace_id=1)
+    a, b = sorted_trace(gg["trace"]), sorted_trace(o["trace"])
+    assert first_divergence(a, b) is None, first_divergence(a, b)
+
+
+@pytest.mark.parametrize("svc", ["det", "exp"])
+def test_tools_lindley_tandem(svc):
+    p = W.tool1(70000, svc=svc)
+    g = W.grid([W.static()], [W.poisson(100000, output=(0, 0))], n_seeds=37, n_requests=700)
+    full_check(p, g)
+    p = W.tandem(60000, 70000, 1000, svc=svc)
+    g = W.grid([W.static("batch")], [W.poisson(100000, output=(0, 0))], n_seeds=37, n_requests=700)
+    full_check(p, g)
+
+
+def test_config1_reduced():
+    # all 8 rates x 3 modes x 3 seeds, N = 1500 (includes TOKEN overflow at high load)
+    p, g = W.config1(n_seeds=3, n_requests=1500)
+    gg, o = full_check(p, g, objective="p99_e2e")
+    st = gg["summary"]["status"]
+    assert (st == 1).any() and (st == 0).any()
+
+
+@pytest.mark.parametrize("obj", ["p50_e2e", "p99_ff", "throughput", "goodput"])
+def test_objectives(obj):
+    p, g = W.config1(n_seeds=2, n_requests=400)
+    full_check(p, g, objective=obj)
+
+
+def test_config2_controller_reduced():
+    p, g = W.config2(n_seeds=3, n_requests=400, series_stride=7, series_windows=64)
+    gg, o = full_check(p, g, series=True)
+    assert gg["summary"]["mode_switches"].sum() > 0
+
+
+def test_config3_routing_batch_control_reduced():
+    p, g = W.config3(n_seeds=2, n_requests=250)
+    gg, o = full_check(p, g)
+    s = gg["summary"]
+    assert s["batch_changes"].sum() > 0 and s["mode_switches"].sum() > 0
+
+
+def test_config4_mmpp_model_selection_reduced():
+    cands = W.config4_candidates()[::331]
+    p, g = W.config4(n_seeds=1, n_requests=300, candidates=cands)
+    gg, o = full_check(p, g, objective="large_under_slo", objective_slo=6_000_000)
+    s = gg["summary"]
+    assert s["select_changes"].sum() > 0 and s["large_items"].sum() > 0
+
+
+def test_config5_policy_mappings_reduced():
+    p, g = W.config5(n_seeds=2, n_requests=300, n_rates=6, n_candidates=70)
+    full_check(p, g)
+
+
+def test_truncation_and_load_metric():
+    p = W.p2_x()
+    cands = [W.adaptive(["function"], metric="load", lo=2000, hi=6000), W.static("batch")]
+    g = W.grid(cands, [W.poisson(m) for m in (998500, 399400)], n_seeds=3, n_requests=600,
+               max_ticks=150_000_000)
+    gg, o = full_check(p, g)
+    assert (gg["summary"]["status"] == 2).any()
+
+
+def test_rank_partition_matches_full_grid():
+    p, g = W.config1(n_seeds=3, n_requests=300)
+    full = run_gpu(p, g)
+    ids = []
+    for rank in range(3):
+        part = run_gpu(p, g, rank=rank, world=3)
+        L = part["res"].layout
+        C = len(g["candidates"])
+        for lg in range(L.n_local_groups):
+            gidx = rank + lg * 3
+            for c in range(C):
+                a = part["summary"][lg * C + c]
+                b = full["summary"][gidx * C + c]
+                assert a.tobytes() == b.tobytes()
+                ids.append(gidx * C + c)
+    assert sorted(ids) == list(range(len(full["summary"])))
+
+
+def test_metrics_derived_fp64():
+    p, g = W.config1(n_seeds=2, n_requests=300, rates=[1, 6])
+    gg = run_gpu(p, g)
+    from paper_2601_03197_b200 import sdas
+    host = {"summary": gg["res"].t["summary"].cpu().numpy()}
+    o = oracle.simulate(p, g)
+    for x in range(len(gg["summary"])):
+        m = sdas.metrics(gg["P"], gg["gv"], host, "replica", x)
+        s = o["summary"][x]
+        if s["status"] != 0:
+            continue
+        n = float(s["completed"])
+        for got, want in ((m["mean_e2e"], float(s["sum_e2e"]) / n), (m["mean_ff"], float(s["sum_ff"]) / n),
+                          (m["throughput"], float(int(s["completed"]) * 10 ** 6) / float(s["makespan"]))):
+            assert abs(got - want) <= 1e-12 * abs(want)

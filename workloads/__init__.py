@@ -128,7 +128,7 @@ def p2_x(mode="function", request_cap=128):
     dev = role("dev", c=cost(h=0), max_num_seqs=16, n_functions=4,
                inbox_cap=request_cap, wait_cap=request_cap)
     tester = role("tester", c=cost(h=20000), max_num_seqs=8, out=(0, 1, 1),
-                  inbox_cap=512, flight_cap=64, wait_cap=512)
+                  inbox_cap=256, flight_cap=64, wait_cap=512)   # wait <= R_cap * F = 512 never overflows
     return pipeline([dev, tester], [link(0, 1, net=1000, chunk=4, mode=mode)],
                     request_cap=request_cap)
 
