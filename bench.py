@@ -1,0 +1,342 @@
+#!/usr/bin/env python
+"""Benchmark of the SDAS strategy-simulation hot path (BASELINE.json metric: simulated message events/s
+and replicas/s at 1/2/4/8 B200, p99 exactness).
+
+Workload at N=1: BASELINE config 2 -- the P2-X developer->tester pipeline with the metrics-driven
+controller switching the message granularity per 1 s window: 64 policies x 8 Poisson rates x 2048
+seeds = 1,048,576 replicas of 1000 requests.  One step = one pass of the whole hot
+path over one batch of fresh synthetic input (seed offset advances every step): K1 simulation with
+in-loop control + metrics + exact percentiles + cell merge, K3 per-group argmin, the NCCL collective
+(N>1), K4/K5 pooled per-rate argmin.  Scaling is weak: each GPU simulates 1M replicas per step.
+
+  python bench.py [--gpus N --steps K --warmup W]          # product (libsdas, sm_100a)
+  python bench.py --impl reference ...                      # the CPU oracle on host cores
+Multi-GPU: python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import workloads as W  # noqa: E402
+
+METRIC = "simulated message events/sec"
+UNIT = "message_events/s"
+ALG_WARP_INSTR_PER_DES_EVENT = 20   # SURVEY.md §8(d.4) algorithmic floor, DESIGN.md §"Roofline"
+
+
+def env_rank():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def workload(args, world):
+    seeds = args.seeds * world                          # weak scaling: args.seeds per GPU
+    pipe, grid = W.config2(n_seeds=seeds, n_requests=args.requests, series_stride=0)
+    return pipe, grid
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.Q,
+                                       "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.f,
+                                      stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        self.f.flush()
+        self.f.seek(0)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.f.read().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx.append(float(parts[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_baseline(args, target_s=15.0):
+    """The oracle as it stands, on this host's cores, on a bounded sample of the same workload."""
+    import oracle
+    pipe, grid = W.config2(n_seeds=args.seeds, n_requests=args.requests, series_stride=0)
+    R = W.grid_size(grid)
+    threads = os.cpu_count() or 1
+    probe = W.sample_ids(R, 128)
+    t0 = time.perf_counter()
+    oracle.simulate(pipe, grid, ids=probe, threads=threads, records=False, hists=False)
+    dt = max(1e-3, time.perf_counter() - t0)
+    n = int(min(R, max(128, 128 * target_s / dt)))
+    ids = W.sample_ids(R, n)
+    t0 = time.perf_counter()
+    o = oracle.simulate(pipe, grid, ids=ids, threads=threads, records=False, hists=False)
+    dt = time.perf_counter() - t0
+    s = o["summary"]
+    msg = int(s["arrivals"].astype(np.int64).sum() + s["deliveries"].astype(np.int64).sum())
+    des = msg + int(s["recv_steps"].astype(np.int64).sum() + s["decode_steps"].astype(np.int64).sum() +
+                    s["window_closes"].astype(np.int64).sum())
+    return {"value": msg / dt, "unit": UNIT, "cores": threads, "kind": "oracle",
+            "sample": "%d of %d config-2 replicas (every floor(R/n)-th id + last), N=%d requests, %.1f s" % (
+                len(ids), R, args.requests, dt),
+            "replicas_per_s": len(ids) / dt, "des_events_per_s": des / dt, "seconds": dt}
+
+
+def run_reference(args):
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return
+    import oracle
+    pipe, grid = W.config2(n_seeds=args.seeds, n_requests=args.requests, series_stride=0)
+    R = W.grid_size(grid)
+    threads = os.cpu_count() or 1
+    per_step = args.ref_sample
+    tot_msg, tot_t, tot_rep = 0, 0.0, 0
+    for k in range(args.warmup + args.steps):
+        ids = (np.asarray(W.sample_ids(R, per_step), dtype=np.uint64) + k) % R   # fresh replicas each step
+        t0 = time.perf_counter()
+        o = oracle.simulate(pipe, grid, ids=ids, threads=threads, records=False, hists=False)
+        dt = time.perf_counter() - t0
+        if k >= args.warmup:
+            s = o["summary"]
+            tot_msg += int(s["arrivals"].astype(np.int64).sum() + s["deliveries"].astype(np.int64).sum())
+            tot_t += dt
+            tot_rep += len(ids)
+    v = tot_msg / tot_t
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1000 * tot_t / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "config": {"workload": "config2: P2-X dev->tester, 64 policies x 8 rates x %d seeds, N=%d (sampled)" % (
+                args.seeds, args.requests), "sample_per_step": per_step},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "oracle",
+                             "sample": "%d replicas per step of %d (config 2)" % (per_step, R)},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "replicas_per_s": tot_rep / tot_t}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="sdas", choices=["sdas", "reference"])
+    ap.add_argument("--seeds", type=int, default=2048, help="seeds per GPU (config 2: 2048 -> 1M replicas)")
+    ap.add_argument("--requests", type=int, default=1000)
+    ap.add_argument("--ref-sample", type=int, default=512)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2601_03197_b200 import parallel, sdas
+
+    rank, world, local = env_rank()
+    assert world == args.gpus, "launch N>1 under torch.distributed.run with --nproc-per-node N"
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    pipe, grid = workload(args, world)
+    P = sdas.Pipeline(pipe)
+    S_total = grid["n_seeds"]
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)     # > 126 MB L2
+    stream = torch.cuda.current_stream(dev)
+
+    def grid_for(step):
+        g = dict(grid)
+        g["seed_offset"] = step * S_total                              # fresh synthetic input per step
+        return g
+
+    gv0 = sdas.GridView(pipe, grid_for(0), rank=rank, world=world)
+    L = sdas.results_layout(P, gv0)
+    res = sdas.Result(L, sdas.allocate(L, dev, 0))
+    acc_local = torch.zeros(sdas.NCNT, dtype=torch.int64, device=dev)
+    acc_global = torch.zeros(sdas.NCNT, dtype=torch.int64, device=dev)
+
+    def one_step(step, timed, ev):
+        gv = sdas.GridView(pipe, grid_for(step), rank=rank, world=world)
+        res.t["cell_cnt"].zero_()
+        res.t["cell_hist"].zero_()
+        flush.fill_(step & 0xFF)                                       # L2 flush before the step
+        ev[0].record(stream)
+        sdas.simulate(P, gv, device=dev, result=res)                   # K1
+        ev[1].record(stream)
+        sdas.group_argmin(P, gv, res, objective="p99_e2e", device=dev)  # K3
+        ev[2].record(stream)
+        cnt_view = res.t["cell_cnt"][: L.n_cells * sdas.NCNT * 8].view(torch.int64).view(L.n_cells, sdas.NCNT)
+        if timed:
+            acc_local.add_(cnt_view.sum(0))
+        ev[3].record(stream)
+        if world > 1:                                                  # the one exchange step
+            parallel.reduce_cells(res)
+            parallel.gather_best_groups(res, L.n_groups, rank, world)
+        ev[4].record(stream)
+        sdas.finalize(P, gv, res, objective="p99_e2e", device=dev)     # K4 + K5
+        ev[5].record(stream)
+        if timed:
+            acc_global.add_(cnt_view.sum(0))
+
+    mk = lambda: [torch.cuda.Event(enable_timing=True) for _ in range(6)]  # noqa: E731
+    for k in range(args.warmup):
+        one_step(1000 + k, False, mk())
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    evs = [mk() for _ in range(args.steps)]
+    for k in range(args.steps):
+        one_step(k, True, evs[k])
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    step_ms = [e[0].elapsed_time(e[5]) - e[2].elapsed_time(e[3]) for e in evs]    # excludes accounting adds
+    k1_ms = [e[0].elapsed_time(e[1]) for e in evs]
+    k3_ms = [e[1].elapsed_time(e[2]) for e in evs]
+    coll_ms = [e[3].elapsed_time(e[4]) for e in evs]
+    fin_ms = [e[4].elapsed_time(e[5]) for e in evs]
+    local_ms = torch.tensor([sum(step_ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(local_ms, op=dist.ReduceOp.MAX)
+    total_ms = float(local_ms.item())
+    loc = acc_local.cpu().numpy()
+    glob = acc_global.cpu().numpy()
+    if world == 1:
+        glob = loc
+    F = {n: i for i, n in enumerate(sdas.CELL_FIELDS)}
+    msg = int(glob[F["arrivals"]] + glob[F["deliveries"]])
+    des = msg + int(glob[F["recv_steps"]] + glob[F["decode_steps"]] + glob[F["window_closes"]])
+    reps = int(glob[F["n_replicas"]])
+    loc_des = int(loc[F["arrivals"]] + loc[F["deliveries"]] + loc[F["recv_steps"]] + loc[F["decode_steps"]] +
+                  loc[F["window_closes"]])
+    value = msg / (total_ms / 1e3)
+
+    # roofline of the dominant kernel K1: integer-issue bound (no tensor cores, HBM traffic << roof)
+    pk = peaks()
+    n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
+    f_mhz = float(pk.get("sm_max_mhz", 1965.0))
+    peak = n_sm * 4 * f_mhz * 1e6 / 1e12                               # warp-instructions per second (x1e12)
+    k1_avg_s = statistics.mean(k1_ms) / 1e3
+    achieved = ALG_WARP_INSTR_PER_DES_EVENT * (loc_des / args.steps) / k1_avg_s / 1e12
+    traffic = None
+    try:
+        prof = json.load(open(os.path.join(ROOT, "profiles", "k1_ncu_summary.json")))
+        if prof.get("dram_bytes_per_des_event") is not None:
+            traffic = prof["dram_bytes_per_des_event"] * (loc_des / args.steps)
+    except Exception:
+        pass
+
+    e2e = None
+    if not args.no_e2e:
+        # end to end through the public API: host descriptors -> H2D (inside sdas_simulate), the whole
+        # sweep + collective, D2H of every result (summaries, cells, best tables) into pinned memory
+        pinned = {n: torch.empty(int(getattr(L, n + "_bytes")), dtype=torch.uint8, pin_memory=True)
+                  for n in ("summary", "cell_cnt", "cell_hist", "best_group", "best_row")}
+        h2d = 0
+        e2e_ms = []
+        for k in range(args.steps):
+            g = grid_for(100 + k)
+            torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            flush.fill_(k & 0xFF)
+            a.record(stream)
+            res.t["cell_cnt"].zero_()
+            res.t["cell_hist"].zero_()
+            r2, table, _, gvk = parallel.sweep(pipe, g, objective="p99_e2e", rank=rank, world=world, device=dev,
+                                                result=res, pipeline=P)
+            for n, h in pinned.items():
+                h.copy_(res.t[n][: h.numel()], non_blocking=True)
+            b.record(stream)
+            b.synchronize()
+            e2e_ms.append(a.elapsed_time(b))
+            h2d = L.params_bytes
+        t = torch.tensor([sum(e2e_ms)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        d2h = sum(h.numel() for h in pinned.values())
+        e2e = {"value": msg / (float(t.item()) / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h)}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "config": {"workload": "config2: P2-X dev->tester, per-1s-window mode control, 64 policies x 8 "
+                                   "Poisson rates x %d seeds/GPU, N=%d requests/replica" % (args.seeds, args.requests),
+                       "replicas_per_step": reps // args.steps, "n_requests": args.requests,
+                       "l2": "flushed (256 MiB write) before every step",
+                       "parallelism": "replica-grid dp%d (group-interleaved), NCCL all_reduce of cells" % world},
+            "replicas_per_s": reps / (total_ms / 1e3),
+            "des_events_per_s": des / (total_ms / 1e3),
+            "phase_ms": {"k1_simulate": statistics.mean(k1_ms), "k3_group_argmin": statistics.mean(k3_ms),
+                         "collective": statistics.mean(coll_ms), "k4k5_finalize": statistics.mean(fin_ms)},
+            "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "warp-instr/s x1e12",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "note": "K1; achieved = %d algorithmic warp-instr per DES event (SURVEY §8d.4 floor) x "
+                                 "DES events / K1 time; peak = %d SMs x 4 issue/clk x %.0f MHz (MEASURED_PEAKS "
+                                 "sm_max_mhz)" % (ALG_WARP_INSTR_PER_DES_EVENT, n_sm, f_mhz)},
+            "gpu_launches": 4 * args.steps,
+            "clocks": clk,
+            "e2e": e2e,
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline(args)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

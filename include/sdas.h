@@ -204,6 +204,12 @@ sdas_status sdas_simulate(const sdas_pipeline* p, const sdas_grid* grid, const s
 sdas_status sdas_control_sweep(const sdas_pipeline* p, const sdas_grid* grid, uint32_t objective,
                                uint64_t objective_slo, const sdas_buffers* dev, void* stream);
 
+/* K3 alone: per-group argmin for `objective` over summaries already written by sdas_simulate /
+ * sdas_control_sweep with the same grid (re-rank candidates under another objective without
+ * re-simulating).  Requires params, summary, best_group. */
+sdas_status sdas_group_argmin(const sdas_pipeline* p, const sdas_grid* grid, uint32_t objective,
+                              uint64_t objective_slo, const sdas_buffers* dev, void* stream);
+
 /* Per-row (i, k) argmin over pooled cells (after the caller's all_reduce of the cell buffers). */
 sdas_status sdas_finalize(const sdas_pipeline* p, const sdas_grid* grid, uint32_t objective,
                           uint64_t objective_slo, const sdas_buffers* dev, void* stream);

@@ -537,6 +537,25 @@ sdas_status sdas_control_sweep(const sdas_pipeline* p, const sdas_grid* grid, ui
   return ok();
 }
 
+sdas_status sdas_group_argmin(const sdas_pipeline* p, const sdas_grid* grid, uint32_t objective,
+                              uint64_t objective_slo, const sdas_buffers* dev, void* stream) {
+  if (objective > SDAS_MAX_LARGE_FRAC_UNDER_SLO) return fail(SDAS_E_INVALID_ARG, "objective: bad enum");
+  if (!dev || !dev->params || !dev->summary || !dev->best_group)
+    return fail(SDAS_E_BUFFER, "group_argmin needs params, summary and best_group");
+  Plan pl;
+  sdas_status s = plan(p, grid, pl);
+  if (s != SDAS_OK) return s;
+  std::vector<uint8_t> blob;
+  pack_blob(grid, pl, blob);
+  cudaError_t e = cudaMemcpyAsync(dev->params, blob.data(), sizeof(DParams), cudaMemcpyHostToDevice,
+                                  reinterpret_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return fail(SDAS_E_CUDA, "params upload: %s", cudaGetErrorString(e));
+  int rc = launch_group_argmin(reinterpret_cast<const uint8_t*>(dev->params), pl.hp, dev, objective, objective_slo,
+                               stream);
+  if (rc) return fail(SDAS_E_CUDA, "K3 launch: %s", cuda_error_string(rc));
+  return ok();
+}
+
 sdas_status sdas_finalize(const sdas_pipeline* p, const sdas_grid* grid, uint32_t objective, uint64_t objective_slo,
                           const sdas_buffers* dev, void* stream) {
   if (objective > SDAS_MAX_LARGE_FRAC_UNDER_SLO) return fail(SDAS_E_INVALID_ARG, "objective: bad enum");

@@ -1,0 +1,64 @@
+"""Multi-GPU driver: replica grids partitioned over the GPUs of one box (BASELINE north_star (5)).
+
+Partition (DESIGN.md §"Multi-GPU"): group g (all C candidates of one (rate, profile, seed)) runs on
+rank g % world -- interleaved so that cheap (saturated) and expensive (low-load) groups spread evenly
+-- and is claimed dynamically by the persistent K1 of that rank.  Whole groups stay on one rank, so the
+per-group argmin (K3) is local.  The one exchange step of the method is merging the per-cell integer
+histograms and counters: ONE all_reduce(SUM) of each integer cell buffer (NCCL over NVLink/NVSwitch),
+plus an all_gather of the per-group best tables.  Integer addition is associative, so the reduced
+cells and every derived argmin are bit-identical for any world size.
+"""
+import numpy as np
+
+from . import sdas
+
+
+def local_group_ids(n_groups, rank, world, group_range=None):
+    """Global group ids handled by `rank` (the partition libsdas applies, sdas_grid.rank/world)."""
+    gb, ge = group_range if group_range is not None else (0, n_groups)
+    first = gb + (rank - gb % world) % world
+    return np.arange(first, ge, world, dtype=np.int64)
+
+
+def reduce_cells(result, group=None):
+    """all_reduce(SUM) of the int64 counters and int32 histograms of every cell (in place)."""
+    import torch.distributed as dist
+    L = result.layout
+    cnt = result.t["cell_cnt"][: L.n_cells * sdas.NCNT * 8].view(dtype=__import__("torch").int64)
+    hist = result.t["cell_hist"][: L.n_cells * 2 * sdas.NBINS * 4].view(dtype=__import__("torch").int32)
+    dist.all_reduce(cnt, op=dist.ReduceOp.SUM, group=group)
+    dist.all_reduce(hist, op=dist.ReduceOp.SUM, group=group)
+
+
+def gather_best_groups(result, n_groups, rank, world, group=None):
+    """all_gather of the per-group best tables -> global int32 table [n_groups] on every rank."""
+    import torch
+    import torch.distributed as dist
+    per = (n_groups + world - 1) // world
+    L = result.layout
+    mine = torch.full((per,), -1, dtype=torch.int32, device=result.t["best_group"].device)
+    n = L.n_local_groups
+    if n:
+        mine[:n] = result.t["best_group"][: n * 4].view(torch.int32)
+    out = [torch.empty_like(mine) for _ in range(world)]
+    dist.all_gather(out, mine, group=group)
+    table = torch.empty(n_groups, dtype=torch.int32, device=mine.device)
+    for r in range(world):
+        ids = torch.as_tensor(local_group_ids(n_groups, r, world), device=mine.device)
+        table[ids] = out[r][: len(ids)]
+    return table
+
+
+def sweep(pipe, grid, objective="p99_e2e", objective_slo=0, rank=0, world=1, device="cuda", group=None,
+          flags=0, result=None, pipeline=None):
+    """One full distributed sweep: K1 + K3 on the local partition, the collective, then K4/K5.
+    Returns (result, global best-group table or None, pipeline, grid view)."""
+    P = pipeline or sdas.Pipeline(pipe)
+    gv = sdas.GridView(pipe, grid, flags=flags, rank=rank, world=world)
+    res = sdas.control_sweep(P, gv, objective=objective, objective_slo=objective_slo, device=device, result=result)
+    table = None
+    if world > 1:
+        reduce_cells(res, group)
+        table = gather_best_groups(res, res.layout.n_groups, rank, world, group)
+    sdas.finalize(P, gv, res, objective=objective, objective_slo=objective_slo, device=device)
+    return res, table, P, gv

@@ -129,8 +129,8 @@ class MetricsOut(C.Structure):
 
 
 EXPORTS = ["sdas_last_error", "sdas_version", "sdas_pipeline_create", "sdas_pipeline_destroy", "sdas_set",
-           "sdas_reset", "sdas_get", "sdas_results_layout", "sdas_simulate", "sdas_control_sweep", "sdas_finalize",
-           "sdas_metrics"]
+           "sdas_reset", "sdas_get", "sdas_results_layout", "sdas_simulate", "sdas_control_sweep",
+           "sdas_group_argmin", "sdas_finalize", "sdas_metrics"]
 
 
 def lib():
@@ -157,6 +157,8 @@ def lib():
                                          C.c_void_p]
         L.sdas_finalize.argtypes = [C.c_void_p, C.POINTER(Grid), C.c_uint32, C.c_uint64, C.POINTER(Buffers),
                                     C.c_void_p]
+        L.sdas_group_argmin.argtypes = [C.c_void_p, C.POINTER(Grid), C.c_uint32, C.c_uint64, C.POINTER(Buffers),
+                                        C.c_void_p]
         L.sdas_metrics.argtypes = [C.c_void_p, C.POINTER(Grid), C.POINTER(Buffers), C.c_uint32, C.c_uint64,
                                    C.POINTER(MetricsOut)]
         for f in EXPORTS:
@@ -378,6 +380,14 @@ def simulate(pipeline, gv, device="cuda", result=None, objective=None, objective
 
 def control_sweep(pipeline, gv, objective="p99_e2e", objective_slo=0, device="cuda", result=None):
     return simulate(pipeline, gv, device=device, result=result, objective=objective, objective_slo=objective_slo)
+
+
+def group_argmin(pipeline, gv, result, objective="p99_e2e", objective_slo=0, device="cuda"):
+    """sdas_group_argmin: K3 alone on summaries already in `result`."""
+    bufs = result.buffers()
+    _check(lib().sdas_group_argmin(pipeline.h, gv.ref(), OBJECTIVES[objective], objective_slo, C.byref(bufs),
+                                   _stream(device)))
+    return result
 
 
 def finalize(pipeline, gv, result, objective="p99_e2e", objective_slo=0, device="cuda"):

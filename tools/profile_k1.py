@@ -1,0 +1,32 @@
+"""One K1 (+K3/K4/K5) launch on a reduced config-2 grid, for ncu captures (not a bench number)."""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import workloads as W  # noqa: E402
+from paper_2601_03197_b200 import sdas  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--seeds", type=int, default=16)
+ap.add_argument("--config", type=int, default=2)
+ap.add_argument("--requests", type=int, default=1000)
+a = ap.parse_args()
+if a.config == 2:
+    pipe, grid = W.config2(n_seeds=a.seeds, n_requests=a.requests, series_stride=0)
+elif a.config == 1:
+    pipe, grid = W.config1(n_seeds=a.seeds, n_requests=a.requests)
+P = sdas.Pipeline(pipe)
+gv = sdas.GridView(pipe, grid)
+r = sdas.control_sweep(P, gv, objective="p99_e2e")
+sdas.finalize(P, gv, r)
+torch.cuda.synchronize()
+cnt, _ = r.cells()
+F = {n: i for i, n in enumerate(sdas.CELL_FIELDS)}
+tot = cnt.sum(0)
+des = int(tot[F["arrivals"]] + tot[F["deliveries"]] + tot[F["recv_steps"]] + tot[F["decode_steps"]] +
+          tot[F["window_closes"]])
+print("replicas", int(tot[F["n_replicas"]]), "des_events", des, "msg_events", int(tot[F["arrivals"]] + tot[F["deliveries"]]),
+      "layout smem/replica", r.layout.smem_per_replica, "wpb", r.layout.warps_per_block, "bps", r.layout.blocks_per_sm)
