@@ -5,7 +5,7 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-LIB = os.path.join(HERE, "libsdas.so")
+LIB = os.environ.get("SDAS_LIB", os.path.join(HERE, "libsdas.so"))   # SDAS_LIB: alternate build (debug)
 SOURCES = [os.path.join(CSRC, "sdas_kernels.cu"), os.path.join(CSRC, "sdas_host.cpp")]
 HEADERS = [os.path.join(CSRC, "sdas_internal.h"), os.path.join(os.path.dirname(HERE), "include", "sdas.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -20,14 +20,17 @@ def needs_build():
     return any(os.path.getmtime(s) > t for s in SOURCES + HEADERS)
 
 
-def build(force=False, verbose=False):
-    if not force and not needs_build():
+def build(force=False, verbose=False, debug=False, out=None):
+    out = out or LIB
+    if not force and out == LIB and not needs_build():
         return LIB
-    cmd = [NVCC] + FLAGS + (["-Xptxas", "-v"] if verbose else []) + ["-o", LIB] + SOURCES
+    flags = [f for f in FLAGS if f not in ("-O3", "-lineinfo")] + ["-G"] if debug else FLAGS
+    cmd = [NVCC] + flags + (["-Xptxas", "-v"] if verbose else []) + ["-o", out] + SOURCES
     subprocess.check_call(cmd, cwd=HERE)
     return LIB
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
-    print(LIB)
+    dbg = "--debug" in sys.argv
+    out = os.path.join(HERE, "libsdas_dbg.so") if dbg else None
+    print(build(force="--force" in sys.argv or dbg, verbose="-v" in sys.argv, debug=dbg, out=out))

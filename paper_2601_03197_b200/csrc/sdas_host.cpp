@@ -88,8 +88,8 @@ sdas_status validate_desc(const sdas_pipeline_desc* d) {
     if (R.max_num_seqs < 1 || R.max_num_seqs > SDAS_MAX_BATCH)
       return fail(SDAS_E_INVALID_FIELD, "roles[%u].max_num_seqs: must be in 1..32", r);
     if (R.out_den < 1) return fail(SDAS_E_INVALID_FIELD, "roles[%u].out_den: must be >= 1", r);
-    if (R.n_functions < 1 || R.n_functions > 65535)
-      return fail(SDAS_E_INVALID_FIELD, "roles[%u].n_functions: must be in 1..65535", r);
+    if (R.n_functions < 1 || R.n_functions > 255)
+      return fail(SDAS_E_INVALID_FIELD, "roles[%u].n_functions: must be in 1..255", r);
     if (R.svc > SDAS_SVC_EXP) return fail(SDAS_E_INVALID_FIELD, "roles[%u].svc: bad enum", r);
     if (R.route > SDAS_ROUTE_SELECT) return fail(SDAS_E_INVALID_FIELD, "roles[%u].route: bad enum", r);
     if (R.route == SDAS_ROUTE_FIXED && R.route_fixed >= R.n_instances)
@@ -270,7 +270,9 @@ sdas_status plan(const sdas_pipeline* p, const sdas_grid* g, Plan& pl) {
     S.n_out++;
     h.role[L.dst_role].in_link = (int32_t)l;
   }
-  for (uint32_t r = 0; r < h.n_roles; ++r) h.role[r].batch_words = 2 + 2 * h.role[r].n_out;
+  h.max_out = 1;
+  for (uint32_t r = 0; r < h.n_roles; ++r) h.max_out = std::max(h.max_out, h.role[r].n_out);
+  for (uint32_t r = 0; r < h.n_roles; ++r) h.role[r].batch_words = 1 + 2 * h.max_out;
 
   // --- shared-memory layout of one warp's replica
   uint64_t o = 256;  // WarpHdr
@@ -278,7 +280,7 @@ sdas_status plan(const sdas_pipeline* p, const sdas_grid* g, Plan& pl) {
   h.off_reqA = (uint32_t)o; o += 8ull * R;
   h.off_reqFF = (uint32_t)o; o += 4ull * R;
   h.off_reqJ = (uint32_t)o; o += 4ull * R;
-  h.off_reqO = (uint32_t)o; o += 2ull * R;
+  h.off_reqO = (uint32_t)o; o += 4ull * R;
   h.off_reqNit = (uint32_t)o; o += 2ull * R;
   h.off_reqOut = (uint32_t)o; o += 2ull * R;
   o = align_up(o, 16);
@@ -315,7 +317,7 @@ sdas_status plan(const sdas_pipeline* p, const sdas_grid* g, Plan& pl) {
     const uint64_t sb = h.off_warps + (uint64_t)wpb * h.smem_per_warp;
     if (sb > smem_cap) break;
     int bps = 0, nsm = 0;
-    if (query_occupancy(wpb, (uint32_t)sb, &bps, &nsm) == 0 && bps > 0) {
+    if (query_occupancy(wpb, (uint32_t)sb, h.max_out, &bps, &nsm) == 0 && bps > 0) {
       have_dev = true;
       n_sm = nsm;
     } else {
@@ -454,7 +456,7 @@ sdas_status sdas_set(sdas_pipeline* p, const char* knob, int64_t value) {
   uint32_t idx;
   if (parse_knob(p, knob, &kind, &idx)) return fail(SDAS_E_UNKNOWN_PARAM, "unknown parameter '%s'", knob);
   static const int64_t lo[5] = {1, 1, 0, 1, 1};
-  static const int64_t hi[5] = {SDAS_MAX_BATCH, 65535, SDAS_TOKEN, 65535, (1ll << 31) - 1};
+  static const int64_t hi[5] = {SDAS_MAX_BATCH, 255, SDAS_TOKEN, 65535, (1ll << 31) - 1};
   if (value < lo[kind] || value > hi[kind])
     return fail(SDAS_E_OUT_OF_RANGE, "value %lld out of range [%lld, %lld] for '%s'", (long long)value,
                 (long long)lo[kind], (long long)hi[kind], knob);

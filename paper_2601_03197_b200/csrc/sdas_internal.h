@@ -56,7 +56,7 @@ struct alignas(16) DParams {
   uint32_t series_slots, series_windows, trace_cap, smem_per_warp;
   uint32_t off_warps;        // byte offset of warp 0's region in the CTA's shared memory
   uint32_t off_reqA, off_reqFF, off_reqJ, off_reqO, off_reqNit, off_reqOut, off_bitmap, off_scratch;
-  uint32_t pad0;
+  uint32_t max_out;
   uint64_t window, slo, max_ticks, master_seed;
   uint64_t first_group, n_local_groups, n_local_replicas, trace_replica;
   uint64_t off_cand, off_arr;
@@ -84,7 +84,8 @@ int launch_group_argmin(const uint8_t* params_dev, const DParams& hp, const sdas
                         uint64_t slo, void* stream);
 int launch_finalize(const uint8_t* params_dev, const DParams& hp, const sdas_buffers* b, uint32_t objective,
                     uint64_t slo, uint64_t n_cells, uint64_t n_rows, void* stream);
-int query_occupancy(uint32_t warps_per_block, uint32_t smem_bytes, int* blocks_per_sm, int* n_sm);
+int query_occupancy(uint32_t warps_per_block, uint32_t smem_bytes, uint32_t maxout, int* blocks_per_sm,
+                    int* n_sm);
 const char* cuda_error_string(int code);
 
 }  // namespace sdas

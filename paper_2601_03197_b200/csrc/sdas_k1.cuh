@@ -1,0 +1,919 @@
+// sdas_k1.cuh -- K1: persistent replica-per-warp simulation kernel (included by sdas_kernels.cu).
+//
+// One warp simulates one replica at a time (rules M0-M20); a warp claims the next local
+// replica with one atomicAdd.  Layout of the work inside a warp:
+//   * uniform replica state (time, arrival generator, counters) in registers, identical in all lanes;
+//   * lane i = instance i: server state (step end, ring indices, batch size, max_num_seqs, window
+//     accumulators) in registers, so the next-event search is one __reduce_min_sync over 32-bit
+//     deltas and the window integration is lane-parallel;
+//   * lane k = batch sequence k of the instance whose DECODE completes: token advance, emission test,
+//     ballot/popc message placement, stable compaction;
+//   * shared memory: request table, per-instance rings (inbox, in-flight, decode-wait), batch words,
+//     controller state; the finalize scratch aliases the (dead) request table.
+// TRACE adds the debug event trace (separate instantiation); MAXOUT is the largest fan-out (1 or 2).
+
+template <bool TRACE, int MAXOUT>
+__global__ void __launch_bounds__(256, 2)
+k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* __restrict__ summary,
+            unsigned long long* __restrict__ records_out, uint8_t* __restrict__ series,
+            long long* __restrict__ cell_cnt, int* __restrict__ cell_hist, uint8_t* __restrict__ trace_buf) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  {
+    const uint4* src = reinterpret_cast<const uint4*>(blob);
+    uint4* dst = reinterpret_cast<uint4*>(smem);
+    for (uint32_t k = threadIdx.x; k < sizeof(DParams) / 16; k += blockDim.x) dst[k] = src[k];
+  }
+  __syncthreads();
+  const DParams& P = *reinterpret_cast<const DParams*>(smem);
+  const int lane = threadIdx.x & 31;
+  const uint32_t wib = threadIdx.x >> 5;
+  uint8_t* const Wr = smem + P.off_warps + wib * P.smem_per_warp;
+  WarpHdr* const H = reinterpret_cast<WarpHdr*>(Wr);
+  unsigned long long* const rA = at<unsigned long long>(Wr, P.off_reqA);
+  uint32_t* const rFF = at<uint32_t>(Wr, P.off_reqFF);
+  uint32_t* const rJ = at<uint32_t>(Wr, P.off_reqJ);
+  uint32_t* const rO = at<uint32_t>(Wr, P.off_reqO);
+  uint16_t* const rNit = at<uint16_t>(Wr, P.off_reqNit);
+  uint16_t* const rOut = at<uint16_t>(Wr, P.off_reqOut);
+  uint32_t* const bitmap = at<uint32_t>(Wr, P.off_bitmap);
+  uint32_t* const scratch = at<uint32_t>(Wr, P.off_scratch);
+
+  // hoisted constants
+  const uint32_t N = P.n_requests, C = P.C, n_inst = P.n_inst, fb_role = P.feedback_role;
+  const uint32_t R_cap = P.request_cap, n_links = P.n_links;
+  const uint32_t W32 = (uint32_t)P.window;
+  const unsigned long long W = P.window, max_ticks = P.max_ticks, slo = P.slo;
+  const uint32_t key0 = (uint32_t)P.master_seed, key1 = (uint32_t)(P.master_seed >> 32);
+  const unsigned long long gwarp = (unsigned long long)blockIdx.x * (blockDim.x >> 5) + wib;
+  unsigned long long* const rec_scratch =
+      reinterpret_cast<unsigned long long*>(reinterpret_cast<uint8_t*>(work) + sizeof(Work)) + gwarp * N;
+  const DCand* const cands = reinterpret_cast<const DCand*>(blob + P.off_cand);
+  const DArr* const arrs = reinterpret_cast<const DArr*>(blob + P.off_arr);
+
+  // lane-resident constants of instance `lane`
+  const bool is_inst = lane < (int)n_inst;
+  const DInst& MI = P.inst[is_inst ? lane : 0];
+  const uint32_t my_role = MI.role;
+  const uint32_t my_inbox_cap = MI.inbox_cap, my_flight_cap = MI.flight_cap, my_wait_cap = MI.wait_cap;
+  uint8_t* const my_inbox = Wr + MI.off_inbox;
+  uint8_t* const my_ftick = Wr + MI.off_ftick;
+  uint8_t* const my_fbody = Wr + MI.off_fbody;
+  const bool my_large = (MI.flags & 1u) != 0;
+
+  for (;;) {
+    unsigned long long x = 0;
+    if (lane == 0) x = atomicAdd(&work->next_replica, 1ull);
+    x = __shfl_sync(FULL, x, 0);
+    if (x >= P.n_local_replicas) break;
+
+    // ---------------------------------------------------------------- replica coordinates (M1)
+    const uint32_t c = (uint32_t)(x % C);
+    const unsigned long long g = P.first_group + (x / C) * P.world;
+    const unsigned long long rid = g * C + c;
+    const uint32_t s_coord = (uint32_t)(g % P.S) + P.seed_offset;
+    const unsigned long long ik = g / P.S;
+    const uint32_t kk = (uint32_t)(ik % P.K), ii = (uint32_t)(ik / P.K);
+    const DCand& cd = cands[c];
+    const DArr& ad = arrs[ii * P.K + kk];
+    const bool trace_on = TRACE && rid == P.trace_replica;
+    const unsigned long long policy_slo = cd.policy_slo;
+    unsigned long long* const rec =
+        (P.flags & SDAS_FLAG_RECORDS) ? records_out + x * (unsigned long long)N : rec_scratch;
+    SeriesRec* ser = nullptr;
+    if ((P.flags & SDAS_FLAG_SERIES) && P.series_stride && rid % P.series_stride == 0 &&
+        rid / P.series_stride < P.series_slots)
+      ser = reinterpret_cast<SeriesRec*>(series) +
+            (rid / P.series_stride) * (unsigned long long)P.series_windows * n_inst;
+
+    // ---------------------------------------------------------------- init
+    // Warp discipline (independent thread scheduling): warp-uniform scalars live in registers or are
+    // lane-distributed; shared scalars are read-modify-written by lane 0 only and broadcast by shfl;
+    // __syncwarp() orders cross-lane shared-memory traffic at phase boundaries.
+    uint32_t modes = 0;                                   // current mode per link, 2 bits each (M16 state)
+    for (uint32_t l = 0; l < n_links; ++l)
+      modes |= (uint32_t)(cd.mode[l] == 255 ? P.link[l].mode : cd.mode[l]) << (2 * l);
+    int32_t qlm = -(1 << 30), q_last_sel = -(1 << 30);   // lane l: last change of link l's mode
+    uint32_t rr_l = 0;                                    // lane r: round-robin counter of role r
+    uint32_t sel_l = lane < (int)P.n_roles ? P.role[lane].large_inst : 0u;  // lane r: SELECT target
+    uint32_t window_closes = 0, mode_switches = 0, batch_changes = 0, select_changes = 0;
+    for (uint32_t w = lane; w < P.bitmap_words; w += 32) {
+      const uint32_t rem = R_cap - w * 32;
+      bitmap[w] = rem >= 32 ? 0xFFFFFFFFu : ((1u << rem) - 1u);
+    }
+    __syncwarp();
+
+    // lane-per-instance server state (M7)
+    unsigned long long cur = 0, acc_qint = 0, acc_lint = 0, tok = 0;
+    uint32_t st = IDLE, end_lo = 0, ih = 0, in = 0, fh = 0, fn = 0, wh = 0, wn = 0, b = 0, fhead = 0;
+    uint32_t Bk = is_inst ? MI.B_default : 1u;
+    int32_t qlB = -(1 << 30);
+    uint32_t acc_busy = 0, acc_maxq = 0, cnt_deliv = 0, cnt_recv = 0, cnt_decode = 0, n_large = 0;
+
+    // uniform replica state
+    unsigned long long t = 0, A_next = 0, nb = W, int_nsys = 0, sum_e2e = 0, sum_ff = 0;
+    uint32_t t_lo = 0, nb_lo = W32, A_lo = 0, jn = 0, P_next = 0, O_next = 0, nsys = 0, completed = 0, wk = 0;
+    uint32_t admitted = 0, dropped = 0, max_e2e = 0, n_sat = 0, good = 0, w_n = 0, w_good = 0, w_half = 0;
+    bool arr_near = false, ovf = false;
+    uint32_t status = SDAS_REPLICA_OK;
+    uint32_t mm_k = 0;
+    unsigned long long mm_end = 0;
+
+    auto trace = [&](uint32_t code, uint32_t a, uint32_t bb, uint32_t cc) {
+      if (TRACE && trace_on && lane == 0) {
+        const unsigned long long k = atomicAdd(reinterpret_cast<unsigned long long*>(trace_buf), 1ull);
+        if (k < P.trace_cap) {
+          TraceRec* r = reinterpret_cast<TraceRec*>(trace_buf + 8) + k;
+          r->tick = t; r->code = code; r->a = a; r->b = bb; r->c = cc;
+        }
+      }
+    };
+    auto trace_lane = [&](uint32_t code, uint32_t a, uint32_t bb, uint32_t cc) {
+      if (TRACE && trace_on) {
+        const unsigned long long k = atomicAdd(reinterpret_cast<unsigned long long*>(trace_buf), 1ull);
+        if (k < P.trace_cap) {
+          TraceRec* r = reinterpret_cast<TraceRec*>(trace_buf + 8) + k;
+          r->tick = t; r->code = code; r->a = a; r->b = bb; r->c = cc;
+        }
+      }
+    };
+
+    // ---------------------------------------------------------------- arrivals (M4, M5)
+    auto advance_epoch = [&]() {
+      ++mm_k;
+      const uint2 w = philox(mm_k, s_coord, 4u << 16, 0u, key0, key1);
+      const unsigned long long d = exp_sample((mm_k & 1) ? ad.soj1 : ad.soj0, w.x);
+      mm_end += d > 0 ? d : 1ull;
+    };
+    auto gen = [&](uint32_t j, unsigned long long A_prev) {
+      const uint32_t kind = ad.kind;
+      if (kind == SDAS_POISSON) {
+        const uint2 w = philox(j, s_coord, 1u << 16, 0u, key0, key1);
+        A_next = A_prev + exp_sample(ad.gap0, w.x);
+      } else if (kind == SDAS_DET) {
+        A_next = (unsigned long long)j * ad.gap0;
+      } else if (kind == SDAS_LIST) {
+        A_next = reinterpret_cast<const unsigned long long*>(blob + ad.list_off)[j];
+      } else {  // MMPP2: restart at epoch edges
+        unsigned long long tt = A_prev;
+        while (mm_end <= tt) advance_epoch();
+        for (;;) {
+          const uint2 w = philox(j, s_coord, 1u << 16, mm_k, key0, key1);
+          const unsigned long long gg = exp_sample((mm_k & 1) ? ad.gap1 : ad.gap0, w.x);
+          if (tt + gg < mm_end) { A_next = tt + gg; break; }
+          tt = mm_end;
+          advance_epoch();
+        }
+      }
+      const uint2 w = philox(j, s_coord, 2u << 16, 0u, key0, key1);
+      P_next = uni(ad.p_lo, ad.p_hi, w.x);
+      O_next = uni(ad.o_lo, ad.o_hi, w.y);
+      arr_near = A_next - t < 0x80000000ull;
+      A_lo = (uint32_t)A_next;
+    };
+    if (ad.kind == SDAS_MMPP2) {
+      const uint2 w = philox(0u, s_coord, 4u << 16, 0u, key0, key1);
+      const unsigned long long d = exp_sample(ad.soj0, w.x);
+      mm_end = d > 0 ? d : 1ull;
+    }
+    if (N > 0) gen(0, 0);
+
+    // ---------------------------------------------------------------- routing (M11)
+    auto route = [&](uint32_t role) -> uint32_t {
+      const DRole& R = P.role[role];
+      if (R.n == 1) return R.first;
+      uint32_t pol = R.route;
+      if ((pol == SDAS_ROUTE_JSQ || pol == SDAS_ROUTE_RR) && cd.route_override != SDAS_ROUTE_NONE)
+        pol = cd.route_override;
+      if (pol == SDAS_ROUTE_RR) {
+        const uint32_t k = __shfl_sync(FULL, rr_l, role);
+        if (lane == (int)role) rr_l = k + 1;
+        return R.first + k % R.n;
+      }
+      if (pol == SDAS_ROUTE_FIXED) return R.first + R.route_fixed;
+      if (pol == SDAS_ROUTE_SELECT) return __shfl_sync(FULL, sel_l, role);
+      uint32_t key = 0xFFFFFFFFu;
+      if (lane >= (int)R.first && lane < (int)(R.first + R.n)) {
+        const uint32_t load = fn + in + (st == RECV ? 1u : 0u) + wn + b;
+        key = (load << 4) | (uint32_t)(lane - R.first);
+      }
+      key = __reduce_min_sync(FULL, key);
+      return R.first + (key & 15u);
+    };
+
+    // one message into destination `dest`'s in-flight ring (uniform; used by the serial paths)
+    auto push_msg = [&](uint32_t l, uint32_t dest, uint32_t slot, uint32_t tokens, uint32_t flags, uint32_t n_in) {
+      const uint32_t net = P.link[l].net;
+      if (TRACE) trace(TR_EMIT, dest, rJ[slot], tokens | ((flags & 1u) << 16) | ((flags >> 1) << 17) | (l << 20));
+      const DInst& D = P.inst[dest];
+      const uint32_t fn_d = __shfl_sync(FULL, fn, dest);
+      if (fn_d >= D.flight_cap) {
+        if (TRACE) trace(TR_OVERFLOW, 1, dest, 0);
+        ovf = true;
+        return;
+      }
+      const uint32_t idx = wrap_add(__shfl_sync(FULL, fh, dest), fn_d, D.flight_cap);
+      const uint32_t tick = t_lo + net;
+      if (lane == 0) {
+        at<uint32_t>(Wr, D.off_ftick)[idx] = tick;
+        at<unsigned long long>(Wr, D.off_fbody)[idx] = make_body(slot, flags, tokens, n_in);
+      }
+      if (lane == (int)dest) {
+        if (fn == 0) fhead = tick;
+        ++fn;
+      }
+    };
+
+    // ---------------------------------------------------------------- completion (M13, M18)
+    auto request_complete = [&](uint32_t slot) {
+      --nsys;
+      const unsigned long long e2e = t - rA[slot];
+      uint32_t f32 = 0;
+      if (lane == 0) f32 = rFF[slot];
+      f32 = __shfl_sync(FULL, f32, 0);
+      const uint32_t e32 = sat32(e2e);
+      if (e2e >= 0xFFFFFFFFull || f32 == 0xFFFFFFFFu) ++n_sat;
+      if (lane == 0) rec[completed] = (unsigned long long)e32 | ((unsigned long long)f32 << 32);
+      ++completed;
+      sum_e2e += e2e;
+      sum_ff += f32;
+      max_e2e = max(max_e2e, e32);
+      good += e2e <= slo ? 1u : 0u;
+      ++w_n;
+      w_good += e2e <= policy_slo ? 1u : 0u;
+      w_half += 2ull * e2e <= policy_slo ? 1u : 0u;
+      if (TRACE) trace(TR_REQ_DONE, rJ[slot], e32, f32);
+      if (lane == 0) bitmap[slot >> 5] |= 1u << (slot & 31);
+    };
+    auto item_done = [&](uint32_t slot) {  // uniform: one item of request `slot` completes
+      uint32_t o = 0;
+      if (lane == 0) {
+        o = rO[slot] - 1u;
+        rO[slot] = o;
+      }
+      o = __shfl_sync(FULL, o, 0);
+      if (o == 0) request_complete(slot);
+    };
+
+    // ---------------------------------------------------------------- phase COMPLETE: RECV (M8, M10)
+    auto complete_recv = [&](uint32_t i) {
+      const DInst& I = P.inst[i];
+      const uint32_t role = I.role;
+      const DRole& R = P.role[role];
+      const unsigned long long body = __shfl_sync(FULL, cur, i);
+      const uint32_t slot = (uint32_t)(body & 0xFFFFu), flags = (uint32_t)(body >> 16) & 0xFFu;
+      if (TRACE) trace(TR_RECV_DONE, i, rJ[slot], flags);
+      uint32_t out = 0;
+      if (flags & F_CLOSES) {
+        if (role == 0) {
+          out = rOut[slot];
+        } else {
+          const uint32_t n_in = (uint32_t)(body >> 48);
+          const unsigned long long prod = (unsigned long long)n_in * R.out_num;
+          const unsigned long long o64 =
+              R.out_fixed + (R.out_den == 1 ? prod
+                                            : (prod < 0xFFFFFFFFull ? (unsigned long long)((uint32_t)prod / R.out_den)
+                                                                    : prod / R.out_den));
+          out = o64 > 65535ull ? 65535u : (uint32_t)o64;
+        }
+      }
+      if (lane == (int)i) {
+        st = IDLE;
+        ++cnt_recv;
+      }
+      if (!(flags & F_CLOSES)) return;
+      if (out > 0) {
+        const uint32_t wn_i = __shfl_sync(FULL, wn, i);
+        if (wn_i >= I.wait_cap) {
+          if (TRACE) trace(TR_OVERFLOW, 2, i, 0);
+          ovf = true;
+          return;
+        }
+        const uint32_t idx = wrap_add(__shfl_sync(FULL, wh, i), wn_i, I.wait_cap);
+        if (lane == 0) at<uint32_t>(Wr, I.off_wait)[idx] = slot | (out << 16);
+        if (lane == (int)i) ++wn;
+        if (TRACE) trace(TR_ITEM_WAIT, i, rJ[slot], out);
+        return;
+      }
+      // tool item (out = 0): one 0-token message per out-link, then complete now (M9)
+      for (uint32_t q = 0; q < R.n_out; ++q) {
+        const uint32_t l = q ? R.out_link1 : R.out_link0;
+        const uint32_t dest = route(P.link[l].dst);
+        if (lane == 0) rO[slot] += 1u;
+        push_msg(l, dest, slot, 0u, F_OPENS | F_CLOSES, 0u);
+        if (ovf) return;
+      }
+      if (lane == 0 && role == fb_role && rFF[slot] == kUnsetFF) rFF[slot] = sat32(t - rA[slot]);
+      if (P.inst[i].flags & 1u) { if (lane == (int)i) ++n_large; }
+      item_done(slot);
+    };
+
+    // ---------------------------------------------------------------- phase COMPLETE: DECODE (M7, M9, M13)
+    auto complete_decode = [&](uint32_t i) {
+      const DInst& I = P.inst[i];
+      const uint32_t role = I.role;
+      const DRole& R = P.role[role];
+      const uint32_t bi = __shfl_sync(FULL, b, i);
+      if (lane == (int)i) {
+        st = IDLE;
+        ++cnt_decode;
+        tok += bi;
+      }
+      if (TRACE) trace(TR_DECODE_DONE, i, bi, 0);
+      uint32_t* const bat = at<uint32_t>(Wr, I.off_batch);
+      const bool act = lane < (int)bi;
+      const uint32_t n_out = R.n_out;
+      uint32_t wA = 0, wB = 0, wD = 0;
+      if (act) {
+        wA = bat[lane];
+        wB = bat[32 + lane];
+        if (MAXOUT > 1) wD = bat[96 + lane];
+      }
+      const uint32_t slot = wA & 0xFFFu, out = wA >> 16;
+      const uint32_t done = (wB & 0xFFFFu) + 1u;
+      wB = (wB & 0xFFFF0000u) | done;
+      // emission test (M9): link q emits when done reaches its next emission point
+      const bool e0 = act && n_out > 0 && done == (wB >> 16);
+      const bool e1 = MAXOUT > 1 && act && n_out > 1 && done == (wD & 0xFFFFu);
+      const uint32_t m0 = __ballot_sync(FULL, e0);
+      const uint32_t m1 = MAXOUT > 1 ? __ballot_sync(FULL, e1) : 0u;
+      uint32_t wC = 0, wE = 0;
+      if (m0 | m1) {
+        if (act) {
+          wC = bat[64 + lane];
+          if (MAXOUT > 1) wE = bat[128 + lane];
+        }
+        for (int q = 0; q < MAXOUT; ++q) {
+          const uint32_t mq = q ? m1 : m0;
+          if (!mq) continue;
+          const bool eq = q ? e1 : e0;
+          const uint32_t l = q ? R.out_link1 : R.out_link0;
+          const uint32_t mode = (wA >> (12 + 2 * q)) & 3u;
+          uint32_t tokens = 0, flags = 0, n_in = 0, sticky = 0;
+          if (eq) {
+            const uint32_t prev = q ? (wD >> 16) : (wC & 0xFFFFu);
+            const uint32_t next = q ? (wD & 0xFFFFu) : (wB >> 16);
+            uint32_t fidx = q ? (wE & 0xFFu) : ((wC >> 16) & 0xFFu);
+            sticky = q ? ((wE >> 8) & 0xFFu) : (wC >> 24);
+            tokens = next - prev;
+            const bool tm = mode == SDAS_TOKEN;
+            flags = (tm ? (prev == 0 ? 1u : 0u) : 1u) | ((tm ? (next == out ? 1u : 0u) : 1u) << 1);
+            n_in = tm ? out : tokens;
+            uint32_t nx = out;
+            if (mode == SDAS_FUNCTION) {
+              ++fidx;
+              const uint32_t Fp = min(R.n_functions, out);
+              nx = min((uint32_t)(((unsigned long long)(fidx + 1u) * out) / Fp), 0xFFFFu);
+            } else if (tm) {
+              nx = min(next + P.link[l].chunk, out);
+            }
+            if (q == 0) {
+              wB = (wB & 0xFFFFu) | (nx << 16);
+              wC = next | (fidx << 16) | (wC & 0xFF000000u);
+            } else {
+              wD = nx | (next << 16);
+              wE = fidx | (wE & 0xFF00u);
+            }
+          }
+          const DRole& Rd = P.role[P.link[l].dst];
+          const uint32_t openers = __ballot_sync(FULL, eq && (flags & 1u));
+          if (Rd.n == 1 || openers == 0) {
+            // every message of this link goes to a known instance: place them in parallel
+            // (per-destination order = batch order; M9/M11 sticky continuations)
+            const uint32_t dest_single = Rd.first;
+            uint32_t dest = (Rd.n == 1 || (flags & 1u)) ? dest_single : sticky;
+            if (Rd.n == 1 && eq && (flags & 1u)) sticky = dest_single;
+            // group lanes by destination (continuations may target different instances)
+            uint32_t todo = mq;
+            while (todo) {
+              const uint32_t dk = __shfl_sync(FULL, dest, __ffs(todo) - 1);
+              const uint32_t grp = __ballot_sync(FULL, eq && dest == dk) & todo;
+              todo &= ~grp;
+              const uint32_t fn_d = __shfl_sync(FULL, fn, dk), fh_d = __shfl_sync(FULL, fh, dk);
+              const DInst& D = P.inst[dk];
+              const uint32_t cnt = __popc(grp);
+              if (fn_d + cnt > D.flight_cap) {
+                if (TRACE) trace(TR_OVERFLOW, 1, dk, 0);
+                ovf = true;
+                return;
+              }
+              const uint32_t tick = t_lo + P.link[l].net;
+              if ((grp >> lane) & 1u) {
+                const uint32_t pos = __popc(grp & lanemask_lt());
+                const uint32_t idx = wrap_add(fh_d, fn_d + pos, D.flight_cap);
+                at<uint32_t>(Wr, D.off_ftick)[idx] = tick;
+                at<unsigned long long>(Wr, D.off_fbody)[idx] = make_body(slot, flags, tokens, n_in);
+                if (flags & 1u) atomicAdd(&rO[slot], 1u);          // M13: +1 per opening message
+                if (TRACE) trace_lane(TR_EMIT, dk, rJ[slot], tokens | ((flags & 1u) << 16) | ((flags >> 1) << 17) | (l << 20));
+              }
+              if (lane == (int)dk) {
+                if (fn == 0) fhead = tick;
+                fn += cnt;
+              }
+            }
+            __syncwarp();
+          } else {
+            // openings need sequential routing (JSQ sees every earlier placement, M11)
+            uint32_t todo = mq;
+            while (todo) {
+              const int k = __ffs(todo) - 1;
+              todo &= todo - 1;
+              const uint32_t fk = __shfl_sync(FULL, flags, k), tk = __shfl_sync(FULL, tokens, k);
+              const uint32_t nk = __shfl_sync(FULL, n_in, k), sk = __shfl_sync(FULL, slot, k);
+              uint32_t dk = __shfl_sync(FULL, sticky, k);
+              if (fk & 1u) {
+                dk = route(P.link[l].dst);
+                if (lane == 0) rO[sk] += 1u;
+                if (lane == k) sticky = dk;
+              }
+              push_msg(l, dk, sk, tk, fk, nk);
+              if (ovf) return;
+            }
+          }
+          if (eq) {
+            if (q == 0) wC = (wC & 0x00FFFFFFu) | (sticky << 24);
+            else wE = (wE & 0xFFu) | (sticky << 8);
+          }
+        }
+      }
+      if (role == fb_role) {  // first output token at a feedback-role instance (M13)
+        if (act && done == 1u && rFF[slot] == kUnsetFF) rFF[slot] = sat32(t - rA[slot]);
+        __syncwarp();
+      }
+      const uint32_t fin = __ballot_sync(FULL, act && done == out);
+      if (!fin) {
+        if (act) {
+          bat[32 + lane] = wB;
+          if (m0 | m1) {
+            bat[64 + lane] = wC;
+            if (MAXOUT > 1) { bat[96 + lane] = wD; bat[128 + lane] = wE; }
+          }
+        }
+        return;
+      }
+      if (lane == (int)i && my_large) n_large += __popc(fin);
+      uint32_t fm = fin;
+      while (fm) {
+        const int k = __ffs(fm) - 1;
+        fm &= fm - 1;
+        item_done(__shfl_sync(FULL, slot, k));
+      }
+      const bool keep = act && done != out;
+      const uint32_t km = __ballot_sync(FULL, keep);
+      if (!(m0 | m1) && act) {
+        wC = bat[64 + lane];
+        if (MAXOUT > 1) wE = bat[128 + lane];
+      }
+      __syncwarp();
+      if (keep) {  // stable compaction
+        const uint32_t nk = __popc(km & lanemask_lt());
+        bat[nk] = wA;
+        bat[32 + nk] = wB;
+        bat[64 + nk] = wC;
+        if (MAXOUT > 1) { bat[96 + nk] = wD; bat[128 + nk] = wE; }
+      }
+      __syncwarp();
+      if (lane == (int)i) b = __popc(km);
+    };
+
+    // ---------------------------------------------------------------- phase START (M7)
+    auto start_recv = [&](uint32_t i) {  // RECV-first: instance i pops its inbox head
+      __syncwarp();                       // rNit / rJ written by other lanes earlier in this tick
+      uint32_t cost32 = 0, slot = 0;
+      if (lane == (int)i) {
+        const unsigned long long body = reinterpret_cast<unsigned long long*>(my_inbox)[ih];
+        slot = (uint32_t)(body & 0xFFFFu);
+        const uint32_t flags = (uint32_t)(body >> 16) & 0xFFu;
+        const uint32_t tokens = (uint32_t)(body >> 32) & 0xFFFFu;
+        unsigned long long cost = (unsigned long long)MI.h + (unsigned long long)MI.beta * tokens;
+        if (flags & F_OPENS) {
+          const uint32_t ord = rNit[slot];
+          rNit[slot] = (uint16_t)(ord + 1u);
+          unsigned long long a = MI.alpha;
+          if (MI.flags & 2u) {
+            const uint2 w = philox(rJ[slot], s_coord, (3u << 16) | my_role, ord, key0, key1);
+            a = exp_sample(MI.alpha, w.x);
+          }
+          cost += a;
+        }
+        if (cost < 1) cost = 1;
+        cost32 = (uint32_t)cost;
+        st = RECV;
+        end_lo = t_lo + cost32;
+        cur = body;
+        ih = wrap_add(ih, 1u, my_inbox_cap);
+        --in;
+      }
+      if (TRACE) trace(TR_RECV_START, i, rJ[__shfl_sync(FULL, slot, i)], __shfl_sync(FULL, cost32, i));
+    };
+    auto start_decode = [&](uint32_t i) {  // FIFO admission (modes bound here, M9) + DECODE step
+      const DInst& I = P.inst[i];
+      const DRole& R = P.role[I.role];
+      const uint32_t bi = __shfl_sync(FULL, b, i), Bi = __shfl_sync(FULL, Bk, i);
+      const uint32_t wn_i = __shfl_sync(FULL, wn, i);
+      const uint32_t nadm = Bi > bi ? min(Bi - bi, wn_i) : 0u;
+      if (nadm) {
+        const uint32_t wh_i = __shfl_sync(FULL, wh, i);
+        uint32_t* const bat = at<uint32_t>(Wr, I.off_batch);
+        if (lane >= (int)bi && lane < (int)(bi + nadm)) {
+          const uint32_t e = at<uint32_t>(Wr, I.off_wait)[wrap_add(wh_i, lane - bi, I.wait_cap)];
+          const uint32_t out = e >> 16;
+          uint32_t wA = (e & 0xFFFu) | (out << 16), wB = 0, wD = 0;
+          for (uint32_t q = 0; q < R.n_out; ++q) {
+            const uint32_t l = q ? R.out_link1 : R.out_link0;
+            const uint32_t mode = (modes >> (2 * l)) & 3u;
+            uint32_t next = out;
+            if (mode == SDAS_FUNCTION) next = out / min(R.n_functions, out);
+            else if (mode == SDAS_TOKEN) next = min(P.link[l].chunk, out);
+            wA |= mode << (12 + 2 * q);
+            if (q == 0) wB = next << 16;
+            else wD = next;
+          }
+          bat[lane] = wA;
+          bat[32 + lane] = wB;
+          bat[64 + lane] = 0xFF000000u;
+          if (MAXOUT > 1) { bat[96 + lane] = wD; bat[128 + lane] = 0xFF00u; }
+        }
+        __syncwarp();
+      }
+      const uint32_t nbat = bi + nadm;
+      uint32_t cost32 = 0;
+      if (lane == (int)i) {
+        wh = wrap_add(wh, nadm, my_wait_cap);
+        wn -= nadm;
+        b = nbat;
+        if (nbat > 0) {
+          unsigned long long cost = (unsigned long long)MI.tau0 + (unsigned long long)MI.gamma * nbat;
+          if (cost < 1) cost = 1;
+          cost32 = (uint32_t)cost;
+          st = DECODE;
+          end_lo = t_lo + cost32;
+        }
+      }
+      if (TRACE && nbat > 0) trace(TR_DECODE_START, i, nbat, __shfl_sync(FULL, cost32, i));
+    };
+
+    // ---------------------------------------------------------------- phase ARRIVE (M14)
+    auto arrive = [&]() {
+      const uint32_t j = jn;
+      if (nsys >= R_cap) {
+        ++dropped;
+        if (TRACE) trace(TR_ARRIVE, j, 0, 0xFFFFFFFFu);
+      } else {
+        ++admitted;
+        ++nsys;
+        __syncwarp();
+        const uint32_t wv = lane < (int)P.bitmap_words ? bitmap[lane] : 0u;   // lowest free slot
+        const uint32_t wm = __ballot_sync(FULL, wv != 0);
+        const int wi = __ffs(wm) - 1;
+        const uint32_t word = __shfl_sync(FULL, wv, wi);
+        const uint32_t bit = __ffs(word) - 1;
+        const uint32_t slot = (uint32_t)wi * 32u + bit;
+        if (lane == 0) {
+          bitmap[wi] = word & ~(1u << bit);
+          rA[slot] = t;
+          rFF[slot] = kUnsetFF;
+          rJ[slot] = j;
+          rO[slot] = 1u;                  // M13: +1 on admission
+          rNit[slot] = 0;
+          rOut[slot] = (uint16_t)O_next;
+        }
+        const uint32_t dest = route(0);
+        if (TRACE) trace(TR_ARRIVE, j, 1, dest);
+        const bool bad = lane == (int)dest && in >= my_inbox_cap;
+        if (lane == (int)dest && !bad) {
+          reinterpret_cast<unsigned long long*>(my_inbox)[wrap_add(ih, in, my_inbox_cap)] =
+              make_body(slot, F_OPENS | F_CLOSES, P_next, P_next);
+          ++in;
+        }
+        if (__ballot_sync(FULL, bad)) {
+          if (TRACE) trace(TR_OVERFLOW, 0, dest, 0);
+          ovf = true;
+        }
+      }
+      ++jn;
+      if (jn < N) gen(jn, t);
+      else arr_near = false;
+    };
+
+    // ---------------------------------------------------------------- window close + control (M15, M16)
+    auto control = [&](int32_t q) {
+      for (uint32_t l = 0; l < n_links; ++l) {  // (i) three-band mode policy
+        if (!((cd.ctl_links >> l) & 1u)) continue;
+        const DRole& Rd = P.role[P.link[l].dst];
+        const bool mine = lane >= (int)Rd.first && lane < (int)(Rd.first + Rd.n);
+        const unsigned long long u =
+            warp_sum64(mine ? (cd.metric_load ? acc_lint : (unsigned long long)acc_busy) : 0ull);
+        const unsigned long long lhs = u * 1000ull;
+        uint32_t band = 1;
+        if (lhs >= (unsigned long long)cd.hi * W * Rd.n) band = 2;
+        else if (lhs <= (unsigned long long)cd.lo * W * Rd.n) band = 0;
+        const uint32_t want = cd.band[band], curm = (modes >> (2 * l)) & 3u;
+        const int32_t ql = __shfl_sync(FULL, qlm, l);
+        if (want != curm && q - ql >= (int32_t)cd.dwell) {
+          modes = (modes & ~(3u << (2 * l))) | (want << (2 * l));
+          if (lane == (int)l) qlm = q;
+          ++mode_switches;
+          if (TRACE) trace(TR_CONTROL, 0, l, want);
+        }
+      }
+      bool viol = false, calm = false;
+      if (w_n >= 1) {
+        const uint32_t k99 = (uint32_t)((99ull * w_n + 99ull) / 100ull);
+        viol = w_good < k99;
+        calm = w_half >= k99;
+      }
+      if (cd.batch_roles && w_n >= 1) {  // (ii) SLO-aware max_num_seqs, lane = instance
+        bool changed = false;
+        if (is_inst && ((cd.batch_roles >> my_role) & 1u)) {
+          uint32_t nbB = Bk;
+          if (viol) nbB = acc_qint > (unsigned long long)cd.q_hi * W ? min(32u, 2u * Bk) : max(1u, Bk / 2u);
+          else if (calm) nbB = MI.B_default;
+          if (nbB != Bk && q - qlB >= (int32_t)cd.dwell) {
+            Bk = nbB;
+            qlB = q;
+            changed = true;
+          }
+        }
+        uint32_t chm = __ballot_sync(FULL, changed);
+        batch_changes += __popc(chm);
+        if (TRACE) {
+          while (chm) {
+            const int k = __ffs(chm) - 1;
+            chm &= chm - 1;
+            trace(TR_CONTROL, 1, k, __shfl_sync(FULL, Bk, k));
+          }
+        }
+      }
+      if (cd.select_role >= 0) {  // (iii) model selection
+        const DRole& Rs = P.role[cd.select_role];
+        const uint32_t cs = __shfl_sync(FULL, sel_l, cd.select_role);
+        const unsigned long long b1000 = (unsigned long long)__shfl_sync(FULL, acc_busy, cs) * 1000ull;
+        uint32_t ns = cs;
+        if (b1000 >= (unsigned long long)cd.hi * W || viol) ns = Rs.small_inst;
+        else if (b1000 <= (unsigned long long)cd.lo * W && !viol) ns = Rs.large_inst;
+        if (ns != cs && q - q_last_sel >= (int32_t)cd.dwell) {
+          if (lane == cd.select_role) sel_l = ns;
+          q_last_sel = q;
+          ++select_changes;
+          if (TRACE) trace(TR_CONTROL, 2, cd.select_role, ns);
+        }
+      }
+    };
+    auto close_window = [&](bool final_partial) {
+      if (ser && wk < P.series_windows && is_inst) {
+        const int32_t il = P.role[my_role].in_link;
+        SeriesRec r;
+        r.qint = acc_qint;
+        r.busy = acc_busy;
+        r.maxq = (uint16_t)min(acc_maxq, 65535u);
+        r.mode = il < 0 ? 255 : (uint8_t)((modes >> (2 * il)) & 3u);
+        r.B = (uint8_t)Bk;
+        ser[(unsigned long long)wk * n_inst + lane] = r;
+      }
+      if (!final_partial) {
+        ++window_closes;
+        if (TRACE) trace(TR_WINDOW, wk, 0, 0);
+        if (cd.adaptive) control((int32_t)wk + 1);
+      }
+      acc_busy = 0; acc_qint = 0; acc_lint = 0; acc_maxq = 0;
+      w_n = 0; w_good = 0; w_half = 0;
+    };
+
+    // ---------------------------------------------------------------- event loop (M12)
+    for (;;) {
+      __syncwarp();
+      if (jn >= N && nsys == 0) break;
+      // next tick: warp-min over 32-bit deltas (every pending event lies < 2^31 ticks ahead)
+      uint32_t d = 0xFFFFFFFFu;
+      if (is_inst) {
+        if (st != IDLE) d = end_lo - t_lo;
+        if (fn) d = min(d, fhead - t_lo);
+      }
+      if (lane == 0) {
+        d = min(d, nb_lo - t_lo);
+        if (arr_near) d = min(d, A_lo - t_lo);
+      }
+      d = __reduce_min_sync(FULL, d);
+      if (max_ticks && t + d > max_ticks) { status = SDAS_REPLICA_TRUNCATED; break; }
+      if (is_inst) {  // integrate the piecewise-constant state over [t, t + d) (M15)
+        const uint32_t Q = in + wn;
+        acc_busy += st != IDLE ? d : 0u;
+        acc_qint += (unsigned long long)Q * d;
+        acc_maxq = max(acc_maxq, Q);
+        acc_lint += (unsigned long long)(fn + Q + (st == RECV ? 1u : 0u) + b) * d;
+      }
+      int_nsys += (unsigned long long)nsys * d;
+      t += d;
+      t_lo += d;
+      if (t_lo == nb_lo) {  // phase 0 WINDOW
+        close_window(false);
+        nb += W;
+        nb_lo += W32;
+        ++wk;
+        if (!arr_near && jn < N) arr_near = A_next - t < 0x80000000ull;
+      }
+      // phase 1 COMPLETE (instance order)
+      const bool done_here = is_inst && st != IDLE && end_lo == t_lo;
+      uint32_t cm = __ballot_sync(FULL, done_here);
+      if (cm) {
+        const uint32_t rm = __ballot_sync(FULL, done_here && st == RECV);
+        do {
+          const int i = __ffs(cm) - 1;
+          cm &= cm - 1;
+          if ((rm >> i) & 1u) complete_recv((uint32_t)i);
+          else complete_decode((uint32_t)i);
+        } while (cm && !ovf);
+        if (ovf) break;
+      }
+      // phase 2 DELIVER (per destination instance, FIFO; lane = instance)
+      const bool dv = is_inst && fn > 0 && fhead == t_lo;
+      if (__ballot_sync(FULL, dv)) {
+        bool lovf = false;
+        if (dv) {
+          const uint32_t* ft = reinterpret_cast<const uint32_t*>(my_ftick);
+          const unsigned long long* fb = reinterpret_cast<const unsigned long long*>(my_fbody);
+          unsigned long long* ib = reinterpret_cast<unsigned long long*>(my_inbox);
+          for (;;) {
+            if (in >= my_inbox_cap) { lovf = true; break; }
+            const unsigned long long body = fb[fh];
+            ib[wrap_add(ih, in, my_inbox_cap)] = body;
+            ++in;
+            fh = wrap_add(fh, 1u, my_flight_cap);
+            --fn;
+            ++cnt_deliv;
+            if (TRACE) trace_lane(TR_DELIVER, lane, rJ[body & 0xFFFFu], (uint32_t)(body >> 32) & 0xFFFFu);
+            if (fn == 0) break;
+            fhead = ft[fh];
+            if (fhead != t_lo) break;
+          }
+        }
+        if (__ballot_sync(FULL, lovf)) {
+          if (TRACE) trace(TR_OVERFLOW, 0, 0, 0);
+          ovf = true;
+          break;
+        }
+        __syncwarp();
+      }
+      // phase 3 ARRIVE (increasing j)
+      if (arr_near && A_lo == t_lo) {
+        do {
+          arrive();
+        } while (!ovf && jn < N && arr_near && A_lo == t_lo);
+        if (ovf) break;
+      }
+      // phase 4 START (idle instances with work, increasing index)
+      __syncwarp();                        // wait-ring / request-table writes of this tick are visible
+      const bool can = is_inst && st == IDLE && (in | wn | b) != 0u;
+      uint32_t sm = __ballot_sync(FULL, can);
+      if (sm) {
+        const uint32_t recvm = __ballot_sync(FULL, can && in != 0u);
+        do {
+          const int i = __ffs(sm) - 1;
+          sm &= sm - 1;
+          if ((recvm >> i) & 1u) start_recv((uint32_t)i);
+          else start_decode((uint32_t)i);
+        } while (sm);
+      }
+    }
+
+    // ---------------------------------------------------------------- finalize (M18, M19)
+    uint8_t* const sum_out = summary + x * SDAS_SUMMARY_BYTES;
+    const unsigned long long cell = ((unsigned long long)ii * P.K + kk) * C + c;
+    uint32_t* const stg = scratch + 2 * SDAS_NBINS + 256;
+    unsigned long long* const cst = reinterpret_cast<unsigned long long*>(stg + 32);
+    __syncwarp();
+    if (ovf) {
+      stg[lane] = 0;
+      __syncwarp();
+      if (lane == 0) {
+        stg[0] = SDAS_REPLICA_OVERFLOW;
+        stg[4] = (uint32_t)t;
+        stg[5] = (uint32_t)(t >> 32);
+        stg[12] = stg[13] = stg[14] = stg[15] = 0xFFFFFFFFu;
+        stg[16] = stg[17] = 0xFFFFFFFFu;
+        stg[31] = (uint32_t)rid;
+      }
+      __syncwarp();
+      if (lane < 8) reinterpret_cast<uint4*>(sum_out)[lane] = reinterpret_cast<const uint4*>(stg)[lane];
+      if (lane == 0) {
+        atomicAdd(reinterpret_cast<unsigned long long*>(cell_cnt + cell * SDAS_NCNT + 0), 1ull);
+        atomicAdd(reinterpret_cast<unsigned long long*>(cell_cnt + cell * SDAS_NCNT + 2), 1ull);
+      }
+      __syncwarp();
+      continue;
+    }
+    close_window(true);  // final partial window: series only
+    uint32_t* const he = scratch;
+    uint32_t* const hf = scratch + SDAS_NBINS;
+    uint32_t* const cnt = scratch + 2 * SDAS_NBINS;
+    for (uint32_t k = lane; k < 2 * SDAS_NBINS; k += 32) he[k] = 0;
+    __syncwarp();
+    for (uint32_t k = lane; k < completed; k += 32) {  // log-bin histograms in shared memory (M17)
+      const unsigned long long v = rec[k];
+      atomicAdd(&he[bin_of((uint32_t)v)], 1u);
+      atomicAdd(&hf[bin_of((uint32_t)(v >> 32))], 1u);
+    }
+    __syncwarp();
+    // exact nearest-rank percentiles: the histogram locates the bin, a radix select inside it (M18)
+    auto select = [&](const uint32_t* h, int field, uint32_t kq, uint32_t& val, uint32_t& binq) {
+      const uint32_t lo_b = lane * 15u, hi_b = min(lo_b + 15u, (uint32_t)SDAS_NBINS);
+      uint32_t part = 0;
+      for (uint32_t bb = lo_b; bb < hi_b; ++bb) part += h[bb];
+      uint32_t incl = warp_incl_scan(part, lane), excl = incl - part;
+      int L = __ffs(__ballot_sync(FULL, incl >= kq && excl < kq)) - 1;
+      uint32_t cum = __shfl_sync(FULL, excl, L);
+      uint32_t bb = (uint32_t)L * 15u;
+      for (;; ++bb) {
+        const uint32_t cc = h[bb];
+        if (cum + cc >= kq) break;
+        cum += cc;
+      }
+      binq = bb;
+      uint32_t r = kq - cum;
+      if (bb < 16u) { val = bb; return; }
+      const uint32_t lo = bin_lo(bb), nbits = (bb - 16u) >> 4;
+      uint32_t prefix = 0;
+      int left = (int)nbits;
+      while (left > 0) {
+        const int db = min(8, left), shift = left - db;
+        for (uint32_t z = lane; z < 256u; z += 32) cnt[z] = 0;
+        __syncwarp();
+        for (uint32_t z = lane; z < completed; z += 32) {
+          const unsigned long long v64 = rec[z];
+          const uint32_t v = field ? (uint32_t)(v64 >> 32) : (uint32_t)v64;
+          const uint32_t off = v - lo;
+          if (v >= lo && (off >> nbits) == 0u && (off >> (shift + db)) == prefix)
+            atomicAdd(&cnt[(off >> shift) & ((1u << db) - 1u)], 1u);
+        }
+        __syncwarp();
+        uint32_t p2 = 0;
+        for (uint32_t z = 8u * lane; z < 8u * lane + 8u; ++z) p2 += cnt[z];
+        incl = warp_incl_scan(p2, lane);
+        excl = incl - p2;
+        L = __ffs(__ballot_sync(FULL, incl >= r && excl < r)) - 1;
+        uint32_t cum2 = __shfl_sync(FULL, excl, L);
+        uint32_t dd = 8u * (uint32_t)L;
+        for (;; ++dd) {
+          const uint32_t cc = cnt[dd];
+          if (cum2 + cc >= r) break;
+          cum2 += cc;
+        }
+        __syncwarp();
+        r -= cum2;
+        prefix = (prefix << db) | dd;
+        left = shift;
+      }
+      val = lo + prefix;
+    };
+    uint32_t v50e = 0xFFFFFFFFu, v99e = 0xFFFFFFFFu, v50f = 0xFFFFFFFFu, v99f = 0xFFFFFFFFu;
+    uint32_t b50e = 0xFFFFu, b99e = 0xFFFFu, b50f = 0xFFFFu, b99f = 0xFFFFu;
+    if (completed > 0) {
+      const uint32_t k50 = (uint32_t)((50ull * completed + 99ull) / 100ull);
+      const uint32_t k99 = (uint32_t)((99ull * completed + 99ull) / 100ull);
+      select(he, 0, k50, v50e, b50e);
+      select(he, 0, k99, v99e, b99e);
+      select(hf, 1, k50, v50f, b50f);
+      select(hf, 1, k99, v99f, b99f);
+    }
+    const uint32_t deliv = __reduce_add_sync(FULL, is_inst ? cnt_deliv : 0u);
+    const uint32_t recvs = __reduce_add_sync(FULL, is_inst ? cnt_recv : 0u);
+    const uint32_t decs = __reduce_add_sync(FULL, is_inst ? cnt_decode : 0u);
+    const uint32_t larges = __reduce_add_sync(FULL, is_inst ? n_large : 0u);
+    const unsigned long long tokens = warp_sum64(is_inst ? tok : 0ull);
+    __syncwarp();
+    if (lane == 0) {
+      const uint32_t arrivals = admitted + dropped;
+      stg[0] = status; stg[1] = admitted; stg[2] = dropped; stg[3] = completed;
+      stg[4] = (uint32_t)t; stg[5] = (uint32_t)(t >> 32);
+      stg[6] = (uint32_t)sum_e2e; stg[7] = (uint32_t)(sum_e2e >> 32);
+      stg[8] = (uint32_t)sum_ff; stg[9] = (uint32_t)(sum_ff >> 32);
+      stg[10] = (uint32_t)int_nsys; stg[11] = (uint32_t)(int_nsys >> 32);
+      stg[12] = v50e; stg[13] = v99e; stg[14] = v50f; stg[15] = v99f;
+      stg[16] = b50e | (b99e << 16); stg[17] = b50f | (b99f << 16);
+      stg[18] = max_e2e; stg[19] = n_sat;
+      stg[20] = arrivals; stg[21] = deliv; stg[22] = recvs; stg[23] = decs;
+      stg[24] = window_closes; stg[25] = mode_switches; stg[26] = good; stg[27] = larges;
+      stg[28] = (uint32_t)tokens; stg[29] = (uint32_t)(tokens >> 32);
+      stg[30] = (batch_changes & 0xFFFFu) | (select_changes << 16);
+      stg[31] = (uint32_t)rid;
+      cst[0] = 1; cst[1] = status == SDAS_REPLICA_OK; cst[2] = 0; cst[3] = status == SDAS_REPLICA_TRUNCATED;
+      cst[4] = admitted; cst[5] = dropped; cst[6] = completed; cst[7] = sum_e2e; cst[8] = sum_ff;
+      cst[9] = t; cst[10] = int_nsys; cst[11] = good; cst[12] = larges; cst[13] = arrivals;
+      cst[14] = deliv; cst[15] = recvs; cst[16] = decs; cst[17] = window_closes; cst[18] = mode_switches;
+      cst[19] = tokens; cst[20] = batch_changes; cst[21] = select_changes; cst[22] = n_sat;
+      cst[23] = 0;
+    }
+    __syncwarp();
+    if (lane < 8) reinterpret_cast<uint4*>(sum_out)[lane] = reinterpret_cast<const uint4*>(stg)[lane];
+    int* const ch = cell_hist + cell * (2 * SDAS_NBINS);
+    for (uint32_t k = lane; k < 2 * SDAS_NBINS; k += 32) {
+      const uint32_t v = he[k];
+      if (v) atomicAdd(ch + k, (int)v);
+    }
+    if (lane < SDAS_NCNT) {
+      const unsigned long long v = cst[lane];
+      if (v) atomicAdd(reinterpret_cast<unsigned long long*>(cell_cnt + cell * SDAS_NCNT + lane), v);
+    }
+    __syncwarp();
+  }
+}
