@@ -42,7 +42,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
   const uint32_t N = P.n_requests, C = P.C, n_inst = P.n_inst, fb_role = P.feedback_role;
   const uint32_t R_cap = P.request_cap, n_links = P.n_links;
   const uint32_t W32 = (uint32_t)P.window;
-  const unsigned long long W = P.window, max_ticks = P.max_ticks, slo = P.slo;
+  const unsigned long long max_ticks = P.max_ticks;
   const uint32_t key0 = (uint32_t)P.master_seed, key1 = (uint32_t)(P.master_seed >> 32);
   const unsigned long long gwarp = (unsigned long long)blockIdx.x * (blockDim.x >> 5) + wib;
   unsigned long long* const rec_scratch =
@@ -69,21 +69,12 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
     // ---------------------------------------------------------------- replica coordinates (M1)
     const uint32_t c = (uint32_t)(x % C);
     const unsigned long long g = P.first_group + (x / C) * P.world;
-    const unsigned long long rid = g * C + c;
     const uint32_t s_coord = (uint32_t)(g % P.S) + P.seed_offset;
-    const unsigned long long ik = g / P.S;
-    const uint32_t kk = (uint32_t)(ik % P.K), ii = (uint32_t)(ik / P.K);
     const DCand& cd = cands[c];
-    const DArr& ad = arrs[ii * P.K + kk];
-    const bool trace_on = TRACE && rid == P.trace_replica;
-    const unsigned long long policy_slo = cd.policy_slo;
+    const DArr& ad = arrs[(g / P.S) % (P.I * (unsigned long long)P.K)];
+    const bool trace_on = TRACE && g * C + c == P.trace_replica;
     unsigned long long* const rec =
         (P.flags & SDAS_FLAG_RECORDS) ? records_out + x * (unsigned long long)N : rec_scratch;
-    SeriesRec* ser = nullptr;
-    if ((P.flags & SDAS_FLAG_SERIES) && P.series_stride && rid % P.series_stride == 0 &&
-        rid / P.series_stride < P.series_slots)
-      ser = reinterpret_cast<SeriesRec*>(series) +
-            (rid / P.series_stride) * (unsigned long long)P.series_windows * n_inst;
 
     // ---------------------------------------------------------------- init
     // Warp discipline (independent thread scheduling): warp-uniform scalars live in registers or are
@@ -95,7 +86,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
     int32_t qlm = -(1 << 30), q_last_sel = -(1 << 30);   // lane l: last change of link l's mode
     uint32_t rr_l = 0;                                    // lane r: round-robin counter of role r
     uint32_t sel_l = lane < (int)P.n_roles ? P.role[lane].large_inst : 0u;  // lane r: SELECT target
-    uint32_t window_closes = 0, mode_switches = 0, batch_changes = 0, select_changes = 0;
+    if (lane == 0) *H = WarpHdr{};
     for (uint32_t w = lane; w < P.bitmap_words; w += 32) {
       const uint32_t rem = R_cap - w * 32;
       bitmap[w] = rem >= 32 ? 0xFFFFFFFFu : ((1u << rem) - 1u);
@@ -110,9 +101,8 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
     uint32_t acc_busy = 0, acc_maxq = 0, cnt_deliv = 0, cnt_recv = 0, cnt_decode = 0, n_large = 0;
 
     // uniform replica state
-    unsigned long long t = 0, A_next = 0, nb = W, int_nsys = 0, sum_e2e = 0, sum_ff = 0;
-    uint32_t t_lo = 0, nb_lo = W32, A_lo = 0, jn = 0, P_next = 0, O_next = 0, nsys = 0, completed = 0, wk = 0;
-    uint32_t admitted = 0, dropped = 0, max_e2e = 0, n_sat = 0, good = 0, w_n = 0, w_good = 0, w_half = 0;
+    unsigned long long t = 0, A_next = 0, int_nsys = 0;
+    uint32_t t_lo = 0, nb_lo = W32, A_lo = 0, jn = 0, P_next = 0, O_next = 0, nsys = 0, wk = 0;
     bool arr_near = false, ovf = false;
     uint32_t status = SDAS_REPLICA_OK;
     uint32_t mm_k = 0;
@@ -226,23 +216,25 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
     // ---------------------------------------------------------------- completion (M13, M18)
     auto request_complete = [&](uint32_t slot) {
       --nsys;
-      const unsigned long long e2e = t - rA[slot];
-      uint32_t f32 = 0;
-      if (lane == 0) f32 = rFF[slot];
-      f32 = __shfl_sync(FULL, f32, 0);
-      const uint32_t e32 = sat32(e2e);
-      if (e2e >= 0xFFFFFFFFull || f32 == 0xFFFFFFFFu) ++n_sat;
-      if (lane == 0) rec[completed] = (unsigned long long)e32 | ((unsigned long long)f32 << 32);
-      ++completed;
-      sum_e2e += e2e;
-      sum_ff += f32;
-      max_e2e = max(max_e2e, e32);
-      good += e2e <= slo ? 1u : 0u;
-      ++w_n;
-      w_good += e2e <= policy_slo ? 1u : 0u;
-      w_half += 2ull * e2e <= policy_slo ? 1u : 0u;
-      if (TRACE) trace(TR_REQ_DONE, rJ[slot], e32, f32);
-      if (lane == 0) bitmap[slot >> 5] |= 1u << (slot & 31);
+      if (lane == 0) {                     // counters and the record: lane 0 owns them
+        const unsigned long long e2e = t - rA[slot];
+        const uint32_t f32 = rFF[slot];
+        const uint32_t e32 = sat32(e2e);
+        WarpHdr& h = *H;
+        if (e2e >= 0xFFFFFFFFull || f32 == 0xFFFFFFFFu) ++h.n_sat;
+        rec[h.completed] = (unsigned long long)e32 | ((unsigned long long)f32 << 32);
+        ++h.completed;
+        h.sum_e2e += e2e;
+        h.sum_ff += f32;
+        h.max_e2e = max(h.max_e2e, e32);
+        h.good += e2e <= P.slo ? 1u : 0u;
+        ++h.w_n;
+        const unsigned long long ps = cd.policy_slo;
+        h.w_good += e2e <= ps ? 1u : 0u;
+        h.w_half += 2ull * e2e <= ps ? 1u : 0u;
+        if (TRACE) trace(TR_REQ_DONE, rJ[slot], e32, f32);
+        bitmap[slot >> 5] |= 1u << (slot & 31);
+      }
     };
     auto item_done = [&](uint32_t slot) {  // uniform: one item of request `slot` completes
       uint32_t o = 0;
@@ -556,10 +548,10 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
     auto arrive = [&]() {
       const uint32_t j = jn;
       if (nsys >= R_cap) {
-        ++dropped;
+        if (lane == 0) ++H->dropped;
         if (TRACE) trace(TR_ARRIVE, j, 0, 0xFFFFFFFFu);
       } else {
-        ++admitted;
+        if (lane == 0) ++H->admitted;
         ++nsys;
         __syncwarp();
         const uint32_t wv = lane < (int)P.bitmap_words ? bitmap[lane] : 0u;   // lowest free slot
@@ -605,28 +597,29 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
             warp_sum64(mine ? (cd.metric_load ? acc_lint : (unsigned long long)acc_busy) : 0ull);
         const unsigned long long lhs = u * 1000ull;
         uint32_t band = 1;
-        if (lhs >= (unsigned long long)cd.hi * W * Rd.n) band = 2;
-        else if (lhs <= (unsigned long long)cd.lo * W * Rd.n) band = 0;
+        if (lhs >= (unsigned long long)cd.hi * P.window * Rd.n) band = 2;
+        else if (lhs <= (unsigned long long)cd.lo * P.window * Rd.n) band = 0;
         const uint32_t want = cd.band[band], curm = (modes >> (2 * l)) & 3u;
         const int32_t ql = __shfl_sync(FULL, qlm, l);
         if (want != curm && q - ql >= (int32_t)cd.dwell) {
           modes = (modes & ~(3u << (2 * l))) | (want << (2 * l));
           if (lane == (int)l) qlm = q;
-          ++mode_switches;
+          if (lane == 0) ++H->mode_switches;
           if (TRACE) trace(TR_CONTROL, 0, l, want);
         }
       }
       bool viol = false, calm = false;
+      const uint32_t w_n = H->w_n;
       if (w_n >= 1) {
         const uint32_t k99 = (uint32_t)((99ull * w_n + 99ull) / 100ull);
-        viol = w_good < k99;
-        calm = w_half >= k99;
+        viol = H->w_good < k99;
+        calm = H->w_half >= k99;
       }
       if (cd.batch_roles && w_n >= 1) {  // (ii) SLO-aware max_num_seqs, lane = instance
         bool changed = false;
         if (is_inst && ((cd.batch_roles >> my_role) & 1u)) {
           uint32_t nbB = Bk;
-          if (viol) nbB = acc_qint > (unsigned long long)cd.q_hi * W ? min(32u, 2u * Bk) : max(1u, Bk / 2u);
+          if (viol) nbB = acc_qint > (unsigned long long)cd.q_hi * P.window ? min(32u, 2u * Bk) : max(1u, Bk / 2u);
           else if (calm) nbB = MI.B_default;
           if (nbB != Bk && q - qlB >= (int32_t)cd.dwell) {
             Bk = nbB;
@@ -635,7 +628,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
           }
         }
         uint32_t chm = __ballot_sync(FULL, changed);
-        batch_changes += __popc(chm);
+        if (lane == 0) H->batch_changes += __popc(chm);
         if (TRACE) {
           while (chm) {
             const int k = __ffs(chm) - 1;
@@ -649,17 +642,24 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
         const uint32_t cs = __shfl_sync(FULL, sel_l, cd.select_role);
         const unsigned long long b1000 = (unsigned long long)__shfl_sync(FULL, acc_busy, cs) * 1000ull;
         uint32_t ns = cs;
-        if (b1000 >= (unsigned long long)cd.hi * W || viol) ns = Rs.small_inst;
-        else if (b1000 <= (unsigned long long)cd.lo * W && !viol) ns = Rs.large_inst;
+        if (b1000 >= (unsigned long long)cd.hi * P.window || viol) ns = Rs.small_inst;
+        else if (b1000 <= (unsigned long long)cd.lo * P.window && !viol) ns = Rs.large_inst;
         if (ns != cs && q - q_last_sel >= (int32_t)cd.dwell) {
           if (lane == cd.select_role) sel_l = ns;
           q_last_sel = q;
-          ++select_changes;
+          if (lane == 0) ++H->select_changes;
           if (TRACE) trace(TR_CONTROL, 2, cd.select_role, ns);
         }
       }
     };
     auto close_window = [&](bool final_partial) {
+      SeriesRec* ser = nullptr;
+      if ((P.flags & SDAS_FLAG_SERIES) && P.series_stride) {
+        const unsigned long long rid = (P.first_group + (x / C) * P.world) * C + c;
+        if (rid % P.series_stride == 0 && rid / P.series_stride < P.series_slots)
+          ser = reinterpret_cast<SeriesRec*>(series) +
+                (rid / P.series_stride) * (unsigned long long)P.series_windows * n_inst;
+      }
       if (ser && wk < P.series_windows && is_inst) {
         const int32_t il = P.role[my_role].in_link;
         SeriesRec r;
@@ -671,12 +671,13 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
         ser[(unsigned long long)wk * n_inst + lane] = r;
       }
       if (!final_partial) {
-        ++window_closes;
+        if (lane == 0) ++H->window_closes;
         if (TRACE) trace(TR_WINDOW, wk, 0, 0);
         if (cd.adaptive) control((int32_t)wk + 1);
       }
       acc_busy = 0; acc_qint = 0; acc_lint = 0; acc_maxq = 0;
-      w_n = 0; w_good = 0; w_half = 0;
+      __syncwarp();
+      if (lane == 0) { H->w_n = 0; H->w_good = 0; H->w_half = 0; }
     };
 
     // ---------------------------------------------------------------- event loop (M12)
@@ -707,7 +708,6 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
       t_lo += d;
       if (t_lo == nb_lo) {  // phase 0 WINDOW
         close_window(false);
-        nb += W;
         nb_lo += W32;
         ++wk;
         if (!arr_near && jn < N) arr_near = A_next - t < 0x80000000ull;
@@ -778,7 +778,8 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
 
     // ---------------------------------------------------------------- finalize (M18, M19)
     uint8_t* const sum_out = summary + x * SDAS_SUMMARY_BYTES;
-    const unsigned long long cell = ((unsigned long long)ii * P.K + kk) * C + c;
+    const unsigned long long rid = g * C + c;
+    const unsigned long long cell = ((g / P.S) % (P.I * (unsigned long long)P.K)) * C + c;
     uint32_t* const stg = scratch + 2 * SDAS_NBINS + 256;
     unsigned long long* const cst = reinterpret_cast<unsigned long long*>(stg + 32);
     __syncwarp();
@@ -803,6 +804,8 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
       continue;
     }
     close_window(true);  // final partial window: series only
+    __syncwarp();
+    const uint32_t completed = H->completed;
     uint32_t* const he = scratch;
     uint32_t* const hf = scratch + SDAS_NBINS;
     uint32_t* const cnt = scratch + 2 * SDAS_NBINS;
@@ -882,6 +885,11 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
     const unsigned long long tokens = warp_sum64(is_inst ? tok : 0ull);
     __syncwarp();
     if (lane == 0) {
+      const WarpHdr& h = *H;
+      const uint32_t admitted = h.admitted, dropped = h.dropped, good = h.good, n_sat = h.n_sat;
+      const unsigned long long sum_e2e = h.sum_e2e, sum_ff = h.sum_ff;
+      const uint32_t window_closes = h.window_closes, mode_switches = h.mode_switches;
+      const uint32_t batch_changes = h.batch_changes, select_changes = h.select_changes;
       const uint32_t arrivals = admitted + dropped;
       stg[0] = status; stg[1] = admitted; stg[2] = dropped; stg[3] = completed;
       stg[4] = (uint32_t)t; stg[5] = (uint32_t)(t >> 32);
@@ -890,7 +898,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
       stg[10] = (uint32_t)int_nsys; stg[11] = (uint32_t)(int_nsys >> 32);
       stg[12] = v50e; stg[13] = v99e; stg[14] = v50f; stg[15] = v99f;
       stg[16] = b50e | (b99e << 16); stg[17] = b50f | (b99f << 16);
-      stg[18] = max_e2e; stg[19] = n_sat;
+      stg[18] = h.max_e2e; stg[19] = n_sat;
       stg[20] = arrivals; stg[21] = deliv; stg[22] = recvs; stg[23] = decs;
       stg[24] = window_closes; stg[25] = mode_switches; stg[26] = good; stg[27] = larges;
       stg[28] = (uint32_t)tokens; stg[29] = (uint32_t)(tokens >> 32);

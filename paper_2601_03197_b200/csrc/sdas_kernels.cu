@@ -35,17 +35,12 @@ struct TraceRec { unsigned long long tick; uint32_t code, a, b, c; };
 struct SeriesRec { unsigned long long qint; uint32_t busy; uint16_t maxq; uint8_t mode, B; };
 static_assert(sizeof(TraceRec) == 24 && sizeof(SeriesRec) == 16, "record sizes");
 
-struct WarpHdr {                        // per-replica scalar state kept in shared memory
-  unsigned long long sum_e2e, sum_ff, int_nsys, tokens;
-  uint32_t admitted, dropped, arrivals, max_e2e;
-  uint32_t n_sat, window_closes, mode_switches, good;
-  uint32_t large_items, batch_changes, select_changes, w_n;
-  uint32_t w_good, w_half, pad0, pad1;
-  uint32_t cur_mode[SDAS_MAX_LINKS + 1];
-  int32_t q_last_mode[SDAS_MAX_LINKS + 1];
-  uint32_t rr[SDAS_MAX_ROLES];
-  uint32_t sel[SDAS_MAX_ROLES];
-  int32_t q_last_sel, pad2, pad3, pad4;
+struct WarpHdr {                        // per-replica counters owned by lane 0 (read by all after __syncwarp)
+  unsigned long long sum_e2e, sum_ff;
+  uint32_t admitted, dropped, completed, max_e2e;
+  uint32_t n_sat, good, w_n, w_good;
+  uint32_t w_half, window_closes, mode_switches, batch_changes;
+  uint32_t select_changes, pad0, pad1, pad2;
 };
 static_assert(sizeof(WarpHdr) <= 256, "WarpHdr");
 
