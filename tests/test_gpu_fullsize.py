@@ -1,0 +1,53 @@
+"""Full-size parity in the launch configuration bench.py times (BASELINE.json configs 1 and 2).
+
+Config 1 (384 replicas x 10,000 requests) is compared in full: every summary, record, cell and both
+argmin tables.  Config 2 (1,048,576 replicas x 1000 requests, in-loop controller) runs entirely on
+the GPU exactly as bench.py runs it (flags 0, one sdas_control_sweep + sdas_finalize); the oracle
+recomputes a deterministic sample of replicas one by one and every summary field must match."""
+import numpy as np
+import pytest
+
+import oracle
+import workloads as W
+from gpu_parity import compare_records, compare_summaries, run_gpu
+from paper_2601_03197_b200 import sdas
+
+pytestmark = pytest.mark.gpu
+
+
+def test_config1_full():
+    p, g = W.config1()
+    gg = run_gpu(p, g, records=True, objective="p99_e2e")
+    sdas.finalize(gg["P"], gg["gv"], gg["res"], objective="p99_e2e")
+    import torch
+    torch.cuda.synchronize()
+    o = oracle.simulate(p, g)
+    compare_summaries(gg["summary"], o["summary"], where="config1")
+    compare_records(gg["records"], o["records"], gg["summary"])
+    cnt, hist = oracle.cells(p, g, o)
+    gcnt, ghist = gg["res"].cells()
+    np.testing.assert_array_equal(gcnt, cnt)
+    np.testing.assert_array_equal(ghist.astype(np.int64), hist)
+    np.testing.assert_array_equal(gg["best_group"], oracle.argmin_groups(p, g, o["summary"], "p99_e2e"))
+    np.testing.assert_array_equal(gg["res"].best_row(), oracle.argmin_rows(p, g, cnt, hist, "p99_e2e"))
+
+
+def test_config2_full_size_sampled():
+    p, g = W.config2(series_stride=0)
+    P = sdas.Pipeline(p)
+    gv = sdas.GridView(p, g)
+    res = sdas.control_sweep(P, gv, objective="p99_e2e")
+    sdas.finalize(P, gv, res, objective="p99_e2e")
+    import torch
+    torch.cuda.synchronize()
+    summ = res.summary()
+    R = W.grid_size(g)
+    assert len(summ) == R == 1 << 20
+    ids = np.asarray(W.sample_ids(R, 384), dtype=np.uint64)
+    o = oracle.simulate(p, g, ids=ids, records=False, hists=False)
+    compare_summaries(summ[ids.astype(np.int64)], o["summary"], where="config2 sample")
+    cnt, _ = res.cells()
+    F = {n: i for i, n in enumerate(sdas.CELL_FIELDS)}
+    assert int(cnt[:, F["n_replicas"]].sum()) == R
+    assert int(cnt[:, F["arrivals"]].sum()) == int(summ["arrivals"].astype(np.int64).sum())
+    assert int(cnt[:, F["mode_switches"]].sum()) == int(summ["mode_switches"].astype(np.int64).sum())
