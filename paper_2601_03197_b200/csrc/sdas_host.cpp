@@ -270,6 +270,9 @@ sdas_status plan(const sdas_pipeline* p, const sdas_grid* g, Plan& pl) {
     S.n_out++;
     h.role[L.dst_role].in_link = (int32_t)l;
   }
+  h.need_lint = 0;
+  for (uint32_t cc = 0; cc < g->n_candidates; ++cc)
+    if (g->cand[cc].kind == SDAS_ADAPTIVE && g->cand[cc].metric == SDAS_METRIC_LOAD) h.need_lint = 1;
   h.max_out = 1;
   for (uint32_t r = 0; r < h.n_roles; ++r) h.max_out = std::max(h.max_out, h.role[r].n_out);
   for (uint32_t r = 0; r < h.n_roles; ++r) h.role[r].batch_words = 1 + 2 * h.max_out;

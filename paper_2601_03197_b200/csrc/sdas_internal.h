@@ -56,7 +56,7 @@ struct alignas(16) DParams {
   uint32_t series_slots, series_windows, trace_cap, smem_per_warp;
   uint32_t off_warps;        // byte offset of warp 0's region in the CTA's shared memory
   uint32_t off_reqA, off_reqFF, off_reqJ, off_reqO, off_reqNit, off_reqOut, off_bitmap, off_scratch;
-  uint32_t max_out;
+  uint32_t max_out, need_lint, pad1, pad2;
   uint64_t window, slo, max_ticks, master_seed;
   uint64_t first_group, n_local_groups, n_local_replicas, trace_replica;
   uint64_t off_cand, off_arr;

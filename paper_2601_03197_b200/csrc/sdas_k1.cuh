@@ -43,6 +43,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
   const uint32_t R_cap = P.request_cap, n_links = P.n_links;
   const uint32_t W32 = (uint32_t)P.window;
   const unsigned long long max_ticks = P.max_ticks;
+  const bool need_lint = P.need_lint != 0;
   const uint32_t key0 = (uint32_t)P.master_seed, key1 = (uint32_t)(P.master_seed >> 32);
   const unsigned long long gwarp = (unsigned long long)blockIdx.x * (blockDim.x >> 5) + wib;
   unsigned long long* const rec_scratch =
@@ -701,7 +702,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
         acc_busy += st != IDLE ? d : 0u;
         acc_qint += (unsigned long long)Q * d;
         acc_maxq = max(acc_maxq, Q);
-        acc_lint += (unsigned long long)(fn + Q + (st == RECV ? 1u : 0u) + b) * d;
+        if (need_lint) acc_lint += (unsigned long long)(fn + Q + (st == RECV ? 1u : 0u) + b) * d;
       }
       int_nsys += (unsigned long long)nsys * d;
       t += d;
@@ -717,12 +718,22 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
       uint32_t cm = __ballot_sync(FULL, done_here);
       if (cm) {
         const uint32_t rm = __ballot_sync(FULL, done_here && st == RECV);
+        // An instance whose inbox stays empty and that receives no delivery / arrival at this tick
+        // takes the same START decision now as in phase 4 (START is invariant for JSQ loads, and
+        // modes / B change only at phase 0), so its next DECODE step is started right away.
+        const uint32_t early = __ballot_sync(FULL, done_here && !(fn > 0 && fhead == t_lo) &&
+                                                       !(my_role == 0 && arr_near && A_lo == t_lo));
         do {
           const int i = __ffs(cm) - 1;
           cm &= cm - 1;
           if ((rm >> i) & 1u) complete_recv((uint32_t)i);
           else complete_decode((uint32_t)i);
-        } while (cm && !ovf);
+          if (ovf) break;
+          if ((early >> i) & 1u) {
+            const uint32_t busy_i = __ballot_sync(FULL, (st != IDLE || in != 0u) && lane == i);
+            if (!busy_i) start_decode((uint32_t)i);
+          }
+        } while (cm);
         if (ovf) break;
       }
       // phase 2 DELIVER (per destination instance, FIFO; lane = instance)
