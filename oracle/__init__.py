@@ -40,6 +40,12 @@ NCNT = 24
 MAX_LINKS = 8
 
 MODES = {"batch": 0, "function": 1, "token": 2}
+KV_POLICIES = {"off": 0, "affinity": 1, "recompute": 2, "posthoc": 3, "hint": 4}
+
+
+def _kv(pipe):
+    kv = pipe.get("kv") or {}
+    return (kv.get("role", 0), kv.get("ctx_tokens", 0), kv.get("tau_xfer", 0), kv.get("home_skew", 0))
 ROUTES = {"jsq": 0, "rr": 1, "fixed": 2, "select": 3}
 ARRIVALS = {"poisson": 0, "mmpp2": 1, "det": 2, "list": 3}
 OBJECTIVES = {"p99_e2e": 0, "p50_e2e": 1, "p99_ff": 2, "throughput": 3, "goodput": 4, "large_under_slo": 5}
@@ -47,7 +53,7 @@ STATUS = {0: "ok", 1: "overflow", 2: "truncated"}
 CELL_FIELDS = ["n_replicas", "n_ok", "n_overflow", "n_truncated", "admitted", "dropped", "completed",
                "sum_e2e", "sum_ff", "makespan_sum", "int_nsys", "good", "large_items", "arrivals",
                "deliveries", "recv_steps", "decode_steps", "window_closes", "mode_switches", "tokens",
-               "batch_changes", "select_changes", "n_saturated", "reserved"]
+               "batch_changes", "select_changes", "n_saturated", "kv_transfers"]
 
 
 def build(force=False):
@@ -84,13 +90,15 @@ class Candidate(C.Structure):
     _fields_ = [("adaptive", C.c_uint32), ("mode", C.c_uint32 * MAX_LINKS), ("ctl_links", C.c_uint32),
                 ("metric_load", C.c_uint32), ("lo", C.c_uint32), ("hi", C.c_uint32), ("dwell", C.c_uint32),
                 ("band", C.c_uint32 * 3), ("route_override", C.c_uint32), ("batch_roles", C.c_uint32),
-                ("q_hi", C.c_uint32), ("select_role", C.c_int32), ("policy_slo", C.c_uint64)]
+                ("q_hi", C.c_uint32), ("select_role", C.c_int32), ("policy_slo", C.c_uint64),
+                ("kv_policy", C.c_uint32)]
 
 
 class Pipeline(C.Structure):
     _fields_ = [("n_roles", C.c_uint32), ("roles", C.POINTER(Role)), ("n_links", C.c_uint32),
                 ("links", C.POINTER(Link)), ("feedback_role", C.c_uint32), ("request_cap", C.c_uint32),
-                ("window", C.c_uint64), ("slo", C.c_uint64), ("link_chunk", C.c_void_p)]
+                ("window", C.c_uint64), ("slo", C.c_uint64), ("kv_role", C.c_uint32),
+                ("kv_ctx_tokens", C.c_uint32), ("kv_tau_xfer", C.c_uint32), ("kv_home_skew", C.c_uint32)]
 
 
 class Grid(C.Structure):
@@ -110,7 +118,7 @@ SUMMARY_FIELDS = [
     ("arrivals", np.uint32), ("deliveries", np.uint32), ("recv_steps", np.uint32), ("decode_steps", np.uint32),
     ("window_closes", np.uint32), ("mode_switches", np.uint32), ("good", np.uint32), ("large_items", np.uint32),
     ("tokens", np.uint64), ("stop_tick", np.uint64), ("replica", np.uint64),
-    ("batch_changes", np.uint32), ("select_changes", np.uint32),
+    ("batch_changes", np.uint32), ("select_changes", np.uint32), ("kv_transfers", np.uint32), ("pad_kv", np.uint32),
     ("msgs_emitted", np.uint64), ("tokens_emitted", np.uint64), ("msgs_received", np.uint64),
     ("tokens_received", np.uint64),
 ]
@@ -195,6 +203,7 @@ def _candidate(c, n_links):
     x.q_hi = c["q_hi"]
     x.select_role = -1 if c["select_role"] is None else c["select_role"]
     x.policy_slo = c["policy_slo"]
+    x.kv_policy = KV_POLICIES[c.get("kv", "off")]
     return x
 
 
@@ -224,7 +233,7 @@ class Problem:
             links[l] = Link(d["src"], d["dst"], d["net"], d["chunk"], MODES[d["mode"]])
         self.pipe = Pipeline(len(pipe["roles"]), C.cast(roles, C.POINTER(Role)), len(pipe["links"]),
                              C.cast(links, C.POINTER(Link)), pipe["feedback_role"], pipe["request_cap"],
-                             pipe["window"], pipe["slo"], None)
+                             pipe["window"], pipe["slo"], *_kv(pipe))
         nl = len(pipe["links"])
         cands = (Candidate * len(grid["candidates"]))(*[_candidate(c, nl) for c in grid["candidates"]])
         I = len(grid["arrivals"])

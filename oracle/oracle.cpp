@@ -204,6 +204,8 @@ enum { TR_ARRIVE = 1, TR_RECV_START, TR_DECODE_START, TR_RECV_DONE, TR_DECODE_DO
 
 struct Msg {
   uint32_t j, dest, link, opens, closes, tokens, n_in;
+  uint32_t kv_kind;   // M23: 0 none, else the KV policy that charges this opening message
+  uint64_t ready;     // M23 HINT: tick at which the hinted transfer completes
 };
 
 struct Event {
@@ -272,6 +274,7 @@ struct Replica {
   std::vector<uint32_t> Pj, Oj;
   std::vector<uint32_t> o, nitems;
   std::vector<uint64_t> ff;
+  std::vector<uint32_t> home;      // M21: KV home instance (index within the KV role) of request j
 
   std::priority_queue<Event, std::vector<Event>, std::greater<Event>> heap;
   uint64_t seq = 0, t = 0;
@@ -290,9 +293,10 @@ struct Replica {
     ++*trace_n;
   }
 
-  uint32_t route(uint32_t role) {  // M11
+  uint32_t route(uint32_t role, uint32_t j) {  // M11 (+ M22 affinity)
     uint32_t n = role_n[role], f = role_first[role];
     if (n == 1) return f;
+    if (P.kv_role && role == P.kv_role && cand.kv_policy == ORC_KV_AFFINITY) return f + home[j];
     const orc_role& R = P.roles[role];
     uint32_t pol = R.route;
     if ((pol == ORC_JSQ || pol == ORC_RR) && cand.route_override != ORC_ROUTE_NONE) pol = cand.route_override;
@@ -314,10 +318,18 @@ struct Replica {
             uint32_t& sticky) {
     const orc_link& L = P.links[l];
     uint32_t dest;
+    uint32_t kv_kind = 0;
+    uint64_t ready = 0;
     if (opens) {
-      dest = route(L.dst);
+      dest = route(L.dst, j);
       sticky = dest;
       o[j] += 1;                                        // M13: +1 per opening message
+      // M23: an opening message routed away from its KV home is charged by the KV policy
+      if (P.kv_role && L.dst == P.kv_role && cand.kv_policy >= ORC_KV_RECOMPUTE &&
+          dest != role_first[L.dst] + home[j]) {
+        kv_kind = cand.kv_policy;
+        ready = t + (uint64_t)P.kv_tau_xfer * P.kv_ctx_tokens;   // hinted transfer starts now
+      }
     } else {
       dest = sticky;
     }
@@ -326,7 +338,7 @@ struct Replica {
     inst[dest].inflight++;
     S.msgs_emitted++;
     S.tokens_emitted += tokens;
-    Event e{t + L.net, PH_DELIVER, ++seq, Msg{j, dest, l, opens, closes, tokens, n_in}};
+    Event e{t + L.net, PH_DELIVER, ++seq, Msg{j, dest, l, opens, closes, tokens, n_in, kv_kind, ready}};
     heap.push(e);
   }
 
@@ -447,6 +459,14 @@ struct Replica {
         }
         cost += a;
       }
+      if (m.opens && m.kv_kind) {  // M23: KV penalty of an opening RECV away from the KV home
+        uint64_t pen;
+        if (m.kv_kind == ORC_KV_RECOMPUTE) pen = (uint64_t)I.c.beta * P.kv_ctx_tokens;
+        else if (m.kv_kind == ORC_KV_POSTHOC) pen = (uint64_t)P.kv_tau_xfer * P.kv_ctx_tokens;
+        else pen = m.ready > t ? m.ready - t : 0;       // HINT: remaining hinted-transfer time
+        cost += pen;
+        S.kv_transfers++;
+      }
       if (cost < 1) cost = 1;
       I.state = RECV;
       I.cur = m;
@@ -484,10 +504,10 @@ struct Replica {
     S.admitted++;
     nsys++;
     o[j] = 1;                       // M13: +1 on admission (the source item)
-    uint32_t dest = route(0);
+    uint32_t dest = route(0, j);
     tr(TR_ARRIVE, j, 1, dest);
     if (inst[dest].inbox.size() >= P.roles[0].inbox_cap) { set_overflow(0, dest); return; }
-    inst[dest].inbox.push_back(Msg{j, dest, 0xFFFFFFFFu, 1, 1, Pj[j], Pj[j]});
+    inst[dest].inbox.push_back(Msg{j, dest, 0xFFFFFFFFu, 1, 1, Pj[j], Pj[j], 0, 0});
   }
 
   void deliver(const Msg& m) {  // phase DELIVER
@@ -644,6 +664,15 @@ struct Replica {
     const orc_arrival& arr = G.arr[r_i * G.n_profiles + r_k];
     if (gen_arrivals(arr, G.master_seed, s_coord, N, A, Pj, Oj) != 0) return -1;
     o.assign(N, 0); nitems.assign(N, 0); ff.assign(N, UINT64_MAX);
+    home.assign(N, 0);
+    if (P.kv_role) {  // M21: KV home of every request, from ATTR words 2 and 3
+      const uint64_t skew32 = ((uint64_t)P.kv_home_skew << 32) / 1000;
+      for (uint32_t j = 0; j < N; ++j) {
+        uint32_t w[4];
+        draw(G.master_seed, j, s_coord, K_ATTR, 0, 0, w);
+        home[j] = (uint64_t)w[2] < skew32 ? 0 : uni(0, role_n[P.kv_role] - 1, w[3]);
+      }
+    }
 
     const uint64_t W = P.window;
     uint64_t next_boundary = W;
@@ -744,6 +773,7 @@ int validate(const orc_pipeline* p, const orc_grid* g) {
   }
   for (uint32_t r = 1; r < p->n_roles; ++r)
     if (indeg[r] != 1) return -1;  // M6: role 0 is the unique source; no joins
+  if (p->kv_role >= p->n_roles || p->kv_home_skew > 1000) return -1;
   for (uint32_t r = 0; r < p->n_roles; ++r) {
     const orc_role& R = p->roles[r];
     if (R.n_instances < 1 || R.max_num_seqs < 1 || R.max_num_seqs > 32 || R.out_den < 1 || R.n_functions < 1)
@@ -848,7 +878,7 @@ void orc_cells(const orc_grid* g, const orc_summary* sums, const uint32_t* hists
     q[9] += x.makespan; q[10] += x.int_nsys; q[11] += x.good; q[12] += x.large_items; q[13] += x.arrivals;
     q[14] += x.deliveries; q[15] += x.recv_steps; q[16] += x.decode_steps; q[17] += x.window_closes;
     q[18] += x.mode_switches; q[19] += x.tokens; q[20] += x.batch_changes; q[21] += x.select_changes;
-    q[22] += x.n_saturated;
+    q[22] += x.n_saturated; q[23] += x.kv_transfers;
     for (int b = 0; b < 2 * ORC_NBINS; ++b) hist[cell * 2 * ORC_NBINS + b] += hists[r * 2 * ORC_NBINS + b];
   }
 }

@@ -21,6 +21,7 @@ enum { ORC_BATCH = 0, ORC_FUNCTION = 1, ORC_TOKEN = 2 };
 enum { ORC_JSQ = 0, ORC_RR = 1, ORC_FIXED = 2, ORC_SELECT = 3, ORC_ROUTE_NONE = 255 };
 enum { ORC_POISSON = 0, ORC_MMPP2 = 1, ORC_DET = 2, ORC_LIST = 3 };
 enum { ORC_OK = 0, ORC_OVERFLOW = 1, ORC_TRUNCATED = 2 };
+enum { ORC_KV_OFF = 0, ORC_KV_AFFINITY = 1, ORC_KV_RECOMPUTE = 2, ORC_KV_POSTHOC = 3, ORC_KV_HINT = 4 };
 enum { ORC_OBJ_P99_E2E = 0, ORC_OBJ_P50_E2E = 1, ORC_OBJ_P99_FF = 2, ORC_OBJ_THROUGHPUT = 3,
        ORC_OBJ_GOODPUT = 4, ORC_OBJ_LARGE_UNDER_SLO = 5 };
 
@@ -62,6 +63,7 @@ typedef struct {
   uint32_t q_hi;
   int32_t select_role;            /* -1 none */
   uint64_t policy_slo;
+  uint32_t kv_policy;             /* ORC_KV_* (rules M21-M24) */
 } orc_candidate;
 
 typedef struct {
@@ -69,7 +71,8 @@ typedef struct {
   uint32_t n_links; const orc_link* links;
   uint32_t feedback_role, request_cap;
   uint64_t window, slo;
-  const uint32_t* link_chunk;     /* unused (chunk from links) */
+  uint32_t kv_role;               /* 0 = no KV modelling; else the role holding per-request KV context */
+  uint32_t kv_ctx_tokens, kv_tau_xfer, kv_home_skew;   /* context tokens, ticks/token, permille on inst 0 */
 } orc_pipeline;
 
 typedef struct {
@@ -91,7 +94,7 @@ typedef struct {
   uint64_t tokens;
   uint64_t stop_tick;
   uint64_t replica;
-  uint32_t batch_changes, select_changes;
+  uint32_t batch_changes, select_changes, kv_transfers, pad_kv;
   uint64_t msgs_emitted, tokens_emitted;     /* conservation checks */
   uint64_t msgs_received, tokens_received;
 } orc_summary;

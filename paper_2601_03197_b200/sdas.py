@@ -43,7 +43,7 @@ TRACE_DTYPE = np.dtype([("tick", "<u8"), ("code", "<u4"), ("a", "<u4"), ("b", "<
 CELL_FIELDS = ["n_replicas", "n_ok", "n_overflow", "n_truncated", "admitted", "dropped", "completed",
                "sum_e2e", "sum_ff", "makespan_sum", "int_nsys", "good", "large_items", "arrivals",
                "deliveries", "recv_steps", "decode_steps", "window_closes", "mode_switches", "tokens",
-               "batch_changes", "select_changes", "n_saturated", "reserved"]
+               "batch_changes", "select_changes", "n_saturated", "kv_transfers"]
 
 
 class SdasError(RuntimeError):

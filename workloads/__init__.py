@@ -300,3 +300,36 @@ def sample_ids(n_total, n_sample=4096):
     step = n_total // n_sample
     ids = sorted(set(list(range(0, n_total, step))[: n_sample - 1] + [n_total - 1]))
     return ids
+
+
+# --------------------------------------------------------------------------------------------
+# f1: KV-cache transfer + controller hints + load balancing (Fig. 6; rules M21-M24)
+# --------------------------------------------------------------------------------------------
+KV_POLICIES = ("affinity", "recompute", "posthoc", "hint")
+
+
+def with_kv(cand, kv):
+    c = dict(cand)
+    c["kv"] = kv
+    return c
+
+
+def p2_kv(ctx_tokens=4000, tau_xfer=20, home_skew=750, request_cap=128):
+    """One software-engineering agent feeding two tester instances that hold per-request KV context
+    ("one instance of the software engineering agent and two instances of the testing
+    agent").  tau_xfer = 0.02 ms/token and prefill 0.05 ms/token as SPEC.md:222; a request's context
+    lives on tester 0 with probability home_skew/1000 (hot sessions), else on a uniform tester."""
+    dev = role("dev", c=cost(h=0), max_num_seqs=32, n_functions=4, inbox_cap=request_cap, wait_cap=request_cap)
+    tester = role("tester", 2, cost(h=1000), max_num_seqs=8, out=(0, 1, 1), route="jsq",
+                  inbox_cap=256, flight_cap=64, wait_cap=256)
+    p = pipeline([dev, tester], [link(0, 1, net=1000, chunk=16, mode="batch")], request_cap=request_cap,
+                 slo=10_000_000)
+    p["kv"] = {"role": 1, "ctx_tokens": ctx_tokens, "tau_xfer": tau_xfer, "home_skew": home_skew}
+    return p
+
+
+def config_kv(n_seeds=8, n_requests=1000, gaps=(1000000, 500000, 350000, 280000, 240000, 210000)):
+    """Simulated Fig. 6: no load balancing (affinity) vs JSQ with recompute / post-hoc transfer /
+    hinted transfer, over request rates."""
+    cands = [with_kv(static("batch"), k) for k in KV_POLICIES]
+    return p2_kv(), grid(cands, [poisson(m) for m in gaps], n_seeds=n_seeds, n_requests=n_requests)
