@@ -51,6 +51,8 @@ enum { SDAS_ROUTE_JSQ = 0, SDAS_ROUTE_RR = 1, SDAS_ROUTE_FIXED = 2, SDAS_ROUTE_S
 enum { SDAS_SVC_DET = 0, SDAS_SVC_EXP = 1 };
 enum { SDAS_POISSON = 0, SDAS_MMPP2 = 1, SDAS_DET = 2, SDAS_LIST = 3 };  /* PAPER.md:38 "varying load" */
 enum { SDAS_STATIC = 0, SDAS_ADAPTIVE = 1 };
+enum { SDAS_KV_OFF = 0, SDAS_KV_AFFINITY = 1, SDAS_KV_RECOMPUTE = 2, SDAS_KV_POSTHOC = 3,
+       SDAS_KV_HINT = 4 };                                              /* PAPER.md:284-290 (Fig. 6) */
 enum { SDAS_METRIC_BUSY = 0, SDAS_METRIC_LOAD = 1 };
 enum { SDAS_REPLICA_OK = 0, SDAS_REPLICA_OVERFLOW = 1, SDAS_REPLICA_TRUNCATED = 2 };
 enum { SDAS_MIN_P99_E2E = 0, SDAS_MIN_P50_E2E = 1, SDAS_MIN_P99_FF = 2, SDAS_MAX_THROUGHPUT = 3,
@@ -109,6 +111,13 @@ typedef struct {
   uint32_t request_cap;                             /* R_cap: admitted-not-completed requests (M14) */
   uint64_t window_ticks;                            /* metrics/control window W (M15), 1..2^31-1 */
   uint64_t slo_ticks;                               /* "good" completions: e2e <= slo (M19) */
+  /* f1 -- KV-cache transfer, controller hints and load balancing (rules M21-M24).
+   * kv_role 0 disables KV modelling; otherwise every request's context (kv_ctx_tokens tokens) lives on
+   * one instance of kv_role (its "home": instance 0 with probability kv_home_skew/1000, else uniform).
+   * An opening message routed away from home pays, at its RECV, beta*ctx (RECOMPUTE), kv_tau_xfer*ctx
+   * (POSTHOC transfer on arrival) or the part of a transfer started at routing time that is still
+   * running (HINT), per the candidate's kv_policy. */
+  uint32_t kv_role, kv_ctx_tokens, kv_tau_xfer, kv_home_skew;
 } sdas_pipeline_desc;
 
 typedef struct sdas_pipeline sdas_pipeline;
@@ -143,6 +152,7 @@ typedef struct {
   uint32_t batch_roles;       /* bitmask of roles with SLO-aware max_num_seqs control (M16(ii)) */
   uint32_t q_hi;              /* M16(ii): grow B when the window's integral Q > q_hi * W */
   int32_t select_role;        /* -1, or the SELECT role driven by model selection (M16(iii)) */
+  uint32_t kv_policy;         /* SDAS_KV_*: routing / KV handling into kv_role (M21-M24) */
   uint64_t policy_slo_ticks;  /* SLO used by the controller's window p99 test */
 } sdas_candidate;
 
@@ -174,7 +184,13 @@ typedef struct {
 typedef struct {
   uint64_t params_bytes;     /* device: packed descriptors (written by the library) */
   uint64_t work_bytes;       /* device: scratch (replica counter + per-warp record scratch) */
-  uint64_t summary_bytes;    /* device: n_local_replicas x 128-byte summary records */
+  uint64_t summary_bytes;    /* device: n_local_replicas x 128-byte summary records, little-endian u32 words:
+                                0 status, 1 admitted, 2 dropped, 3 completed, 4-5 makespan (or overflow tick),
+                                6-7 sum e2e, 8-9 sum ff, 10-11 integral N_sys dt, 12-15 p50/p99 e2e, p50/p99 ff,
+                                16-17 their bins (u16 pairs), 18 max e2e, 19 saturated records, 20 arrivals,
+                                21 deliveries, 22 RECV steps, 23 DECODE steps, 24 window closes, 25 mode
+                                switches, 26 good, 27 large-model items, 28-29 output tokens, 30 batch|select
+                                changes (u16 pair), 31 KV transfers (M24) */
   uint64_t records_bytes;    /* device: n_local_replicas x n_requests x {u32 e2e, u32 ff} (FLAG_RECORDS) */
   uint64_t series_bytes;     /* device: series_slots x series_windows x n_instances x 16 B (FLAG_SERIES) */
   uint64_t cell_cnt_bytes;   /* device: n_cells x SDAS_NCNT int64 (zeroed by the caller; accumulated) */

@@ -61,6 +61,7 @@ struct sdas_pipeline {
   std::vector<sdas_link_desc> links;
   uint32_t feedback_role = 0, request_cap = 0;
   uint64_t window = 0, slo = 0;
+  uint32_t kv_role = 0, kv_ctx = 0, kv_tau = 0, kv_skew = 0;   // f1 (M21-M24)
   // knob registry: current values and registered defaults (Table 1)
   std::vector<uint32_t> B_cur, B_def, F_cur, F_def;
   std::vector<uint32_t> mode_cur, mode_def, chunk_cur, chunk_def, net_cur, net_def;
@@ -78,6 +79,11 @@ sdas_status validate_desc(const sdas_pipeline_desc* d) {
   if (d->feedback_role >= d->n_roles) return fail(SDAS_E_INVALID_FIELD, "feedback_role: out of range");
   if (d->request_cap < 1 || d->request_cap > 4096)
     return fail(SDAS_E_INVALID_FIELD, "request_cap: must be in 1..4096");
+  if (d->kv_role >= d->n_roles) return fail(SDAS_E_INVALID_FIELD, "kv_role: must be 0 (off) or a non-source role");
+  if (d->kv_home_skew > 1000) return fail(SDAS_E_INVALID_FIELD, "kv_home_skew: permille in 0..1000");
+  if (d->kv_role && ((uint64_t)d->kv_ctx_tokens * d->kv_tau_xfer >= (1ull << 30) ||
+                     (uint64_t)d->kv_ctx_tokens * (1u << 15) >= (1ull << 40)))
+    return fail(SDAS_E_INVALID_FIELD, "kv_ctx_tokens/kv_tau_xfer: transfer must stay below 2^30 ticks");
   if (d->window_ticks < 1 || d->window_ticks >= (1ull << 31))
     return fail(SDAS_E_INVALID_FIELD, "window_ticks: must be in 1..2^31-1");
   uint32_t n_inst = 0;
@@ -270,6 +276,12 @@ sdas_status plan(const sdas_pipeline* p, const sdas_grid* g, Plan& pl) {
     S.n_out++;
     h.role[L.dst_role].in_link = (int32_t)l;
   }
+  h.kv_role = p->kv_role;
+  h.kv_ctx = p->kv_ctx;
+  h.kv_tau = p->kv_tau;
+  h.kv_skew32 = ((uint64_t)p->kv_skew << 32) / 1000;
+  for (uint32_t cc = 0; cc < g->n_candidates; ++cc)
+    if (g->cand[cc].kv_policy > SDAS_KV_HINT) return fail(SDAS_E_INVALID_FIELD, "cand[%u].kv_policy: bad enum", cc);
   h.need_lint = 0;
   for (uint32_t cc = 0; cc < g->n_candidates; ++cc)
     if (g->cand[cc].kind == SDAS_ADAPTIVE && g->cand[cc].metric == SDAS_METRIC_LOAD) h.need_lint = 1;
@@ -286,12 +298,14 @@ sdas_status plan(const sdas_pipeline* p, const sdas_grid* g, Plan& pl) {
   h.off_reqO = (uint32_t)o; o += 4ull * R;
   h.off_reqNit = (uint32_t)o; o += 2ull * R;
   h.off_reqOut = (uint32_t)o; o += 2ull * R;
+  h.off_reqHome = (uint32_t)o; o += R;                    // u8 KV home per request slot (M21)
   o = align_up(o, 16);
   h.off_bitmap = (uint32_t)o; o += 4ull * h.bitmap_words;
   for (uint32_t i = 0; i < h.n_inst; ++i) {
     DInst& I = h.inst[i];
     o = align_up(o, 16);
     I.off_inbox = (uint32_t)o; o += 8ull * I.inbox_cap;
+    if (h.kv_role && I.role == h.kv_role) o += 4ull * I.inbox_cap;  // hinted-transfer ready ticks (M23)
     o = align_up(o, 16);
     I.off_ftick = (uint32_t)o; o += 4ull * I.flight_cap;
     o = align_up(o, 16);
@@ -363,6 +377,7 @@ void pack_blob(const sdas_grid* g, const Plan& pl, std::vector<uint8_t>& blob) {
     for (int k = 0; k < 4; ++k) d.band[k] = s.band_mode[k];
     d.route_override = s.route_override; d.batch_roles = s.batch_roles; d.q_hi = s.q_hi;
     d.select_role = s.select_role; d.policy_slo = s.policy_slo_ticks;
+    d.kv_policy = s.kv_policy;
   }
   const uint64_t nIK = (uint64_t)g->n_rates * g->n_profiles;
   DArr* da = reinterpret_cast<DArr*>(blob.data() + pl.hp.off_arr);
@@ -447,6 +462,10 @@ sdas_status sdas_pipeline_create(const sdas_pipeline_desc* desc, sdas_pipeline**
   p->request_cap = desc->request_cap;
   p->window = desc->window_ticks;
   p->slo = desc->slo_ticks;
+  p->kv_role = desc->kv_role;
+  p->kv_ctx = desc->kv_ctx_tokens;
+  p->kv_tau = desc->kv_tau_xfer;
+  p->kv_skew = desc->kv_home_skew;
   *out = p;
   return ok();
 }

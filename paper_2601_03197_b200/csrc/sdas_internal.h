@@ -38,6 +38,7 @@ struct DCand {          // one candidate, 64 B
   uint8_t band[4];
   uint32_t route_override, batch_roles, q_hi;
   int32_t select_role;
+  uint32_t kv_policy;
   uint64_t policy_slo;
 };
 
@@ -56,7 +57,8 @@ struct alignas(16) DParams {
   uint32_t series_slots, series_windows, trace_cap, smem_per_warp;
   uint32_t off_warps;        // byte offset of warp 0's region in the CTA's shared memory
   uint32_t off_reqA, off_reqFF, off_reqJ, off_reqO, off_reqNit, off_reqOut, off_bitmap, off_scratch;
-  uint32_t max_out, need_lint, pad1, pad2;
+  uint32_t max_out, need_lint, kv_role, kv_ctx, kv_tau, off_reqHome;
+  uint64_t kv_skew32;         // M21: home = instance 0 iff ATTR.w2 < kv_skew32 = floor(skew * 2^32 / 1000)
   uint64_t window, slo, max_ticks, master_seed;
   uint64_t first_group, n_local_groups, n_local_replicas, trace_replica;
   uint64_t off_cand, off_arr;

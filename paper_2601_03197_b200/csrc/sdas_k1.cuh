@@ -60,6 +60,13 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
   uint8_t* const my_ftick = Wr + MI.off_ftick;
   uint8_t* const my_fbody = Wr + MI.off_fbody;
   const bool my_large = (MI.flags & 1u) != 0;
+  // f1 (M21-M24): KV-role instances keep, per inbox entry, the tick a hinted transfer completes
+  const uint32_t kv_role = P.kv_role;
+  const bool my_kv = kv_role != 0 && is_inst && my_role == kv_role;
+  uint32_t* const my_iready = reinterpret_cast<uint32_t*>(my_inbox + 8u * my_inbox_cap);
+  const uint32_t my_hint_off =
+      my_kv ? P.kv_tau * P.kv_ctx - P.link[P.role[kv_role].in_link].net : 0u;   // ready = delivery + this
+  uint8_t* const rHome = Wr + P.off_reqHome;
 
   for (;;) {
     unsigned long long x = 0;
@@ -99,7 +106,8 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
     uint32_t st = IDLE, end_lo = 0, ih = 0, in = 0, fh = 0, fn = 0, wh = 0, wn = 0, b = 0, fhead = 0;
     uint32_t Bk = is_inst ? MI.B_default : 1u;
     int32_t qlB = -(1 << 30);
-    uint32_t acc_busy = 0, acc_maxq = 0, cnt_deliv = 0, cnt_recv = 0, cnt_decode = 0, n_large = 0;
+    uint32_t acc_busy = 0, acc_maxq = 0, cnt_deliv = 0, cnt_recv = 0, cnt_decode = 0, n_large = 0, cnt_kv = 0;
+    uint32_t H_next = 0;   // KV home (index within kv_role) of the next arriving request (M21)
 
     // uniform replica state
     unsigned long long t = 0, A_next = 0, int_nsys = 0;
@@ -155,9 +163,10 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
           advance_epoch();
         }
       }
-      const uint2 w = philox(j, s_coord, 2u << 16, 0u, key0, key1);
+      const uint4 w = philox4(j, s_coord, 2u << 16, 0u, key0, key1);
       P_next = uni(ad.p_lo, ad.p_hi, w.x);
       O_next = uni(ad.o_lo, ad.o_hi, w.y);
+      if (kv_role) H_next = (unsigned long long)w.z < P.kv_skew32 ? 0u : uni(0u, P.role[kv_role].n - 1u, w.w);
       arr_near = A_next - t < 0x80000000ull;
       A_lo = (uint32_t)A_next;
     };
@@ -169,9 +178,10 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
     if (N > 0) gen(0, 0);
 
     // ---------------------------------------------------------------- routing (M11)
-    auto route = [&](uint32_t role) -> uint32_t {
+    auto route = [&](uint32_t role, uint32_t slot) -> uint32_t {
       const DRole& R = P.role[role];
       if (R.n == 1) return R.first;
+      if (kv_role && role == kv_role && cd.kv_policy == SDAS_KV_AFFINITY) return R.first + rHome[slot];  // M22
       uint32_t pol = R.route;
       if ((pol == SDAS_ROUTE_JSQ || pol == SDAS_ROUTE_RR) && cd.route_override != SDAS_ROUTE_NONE)
         pol = cd.route_override;
@@ -190,11 +200,17 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
       key = __reduce_min_sync(FULL, key);
       return R.first + (key & 15u);
     };
+    // M23: the KV policy charged to an opening message on link l placed at `dest` (0 = none)
+    auto kv_kind = [&](uint32_t l, uint32_t dest, uint32_t slot) -> uint32_t {
+      if (!kv_role || P.link[l].dst != kv_role || cd.kv_policy < SDAS_KV_RECOMPUTE) return 0u;
+      return dest != P.role[kv_role].first + rHome[slot] ? cd.kv_policy : 0u;
+    };
 
     // one message into destination `dest`'s in-flight ring (uniform; used by the serial paths)
     auto push_msg = [&](uint32_t l, uint32_t dest, uint32_t slot, uint32_t tokens, uint32_t flags, uint32_t n_in) {
       const uint32_t net = P.link[l].net;
-      if (TRACE) trace(TR_EMIT, dest, rJ[slot], tokens | ((flags & 1u) << 16) | ((flags >> 1) << 17) | (l << 20));
+      if (TRACE)
+        trace(TR_EMIT, dest, rJ[slot], tokens | ((flags & 1u) << 16) | (((flags >> 1) & 1u) << 17) | (l << 20));
       const DInst& D = P.inst[dest];
       const uint32_t fn_d = __shfl_sync(FULL, fn, dest);
       if (fn_d >= D.flight_cap) {
@@ -290,9 +306,9 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
       // tool item (out = 0): one 0-token message per out-link, then complete now (M9)
       for (uint32_t q = 0; q < R.n_out; ++q) {
         const uint32_t l = q ? R.out_link1 : R.out_link0;
-        const uint32_t dest = route(P.link[l].dst);
+        const uint32_t dest = route(P.link[l].dst, slot);
         if (lane == 0) rO[slot] += 1u;
-        push_msg(l, dest, slot, 0u, F_OPENS | F_CLOSES, 0u);
+        push_msg(l, dest, slot, 0u, F_OPENS | F_CLOSES | (kv_kind(l, dest, slot) << 2), 0u);
         if (ovf) return;
       }
       if (lane == 0 && role == fb_role && rFF[slot] == kUnsetFF) rFF[slot] = sat32(t - rA[slot]);
@@ -396,7 +412,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
                 at<uint32_t>(Wr, D.off_ftick)[idx] = tick;
                 at<unsigned long long>(Wr, D.off_fbody)[idx] = make_body(slot, flags, tokens, n_in);
                 if (flags & 1u) atomicAdd(&rO[slot], 1u);          // M13: +1 per opening message
-                if (TRACE) trace_lane(TR_EMIT, dk, rJ[slot], tokens | ((flags & 1u) << 16) | ((flags >> 1) << 17) | (l << 20));
+                if (TRACE) trace_lane(TR_EMIT, dk, rJ[slot], tokens | ((flags & 1u) << 16) | (((flags >> 1) & 1u) << 17) | (l << 20));
               }
               if (lane == (int)dk) {
                 if (fn == 0) fhead = tick;
@@ -413,12 +429,14 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
               const uint32_t fk = __shfl_sync(FULL, flags, k), tk = __shfl_sync(FULL, tokens, k);
               const uint32_t nk = __shfl_sync(FULL, n_in, k), sk = __shfl_sync(FULL, slot, k);
               uint32_t dk = __shfl_sync(FULL, sticky, k);
+              uint32_t fkv = fk;
               if (fk & 1u) {
-                dk = route(P.link[l].dst);
+                dk = route(P.link[l].dst, sk);
                 if (lane == 0) rO[sk] += 1u;
                 if (lane == k) sticky = dk;
+                fkv |= kv_kind(l, dk, sk) << 2;
               }
-              push_msg(l, dk, sk, tk, fk, nk);
+              push_msg(l, dk, sk, tk, fkv, nk);
               if (ovf) return;
             }
           }
@@ -487,6 +505,15 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
             a = exp_sample(MI.alpha, w.x);
           }
           cost += a;
+          const uint32_t kvk = (flags >> 2) & 7u;
+          if (kvk) {  // M23: KV penalty of an opening RECV away from the request's KV home
+            uint32_t pen;
+            if (kvk == SDAS_KV_RECOMPUTE) pen = MI.beta * P.kv_ctx;
+            else if (kvk == SDAS_KV_POSTHOC) pen = P.kv_tau * P.kv_ctx;
+            else pen = (uint32_t)max(0, (int32_t)(my_iready[ih] - t_lo));
+            cost += pen;
+            ++cnt_kv;
+          }
         }
         if (cost < 1) cost = 1;
         cost32 = (uint32_t)cost;
@@ -569,8 +596,9 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
           rO[slot] = 1u;                  // M13: +1 on admission
           rNit[slot] = 0;
           rOut[slot] = (uint16_t)O_next;
+          rHome[slot] = (uint8_t)H_next;
         }
-        const uint32_t dest = route(0);
+        const uint32_t dest = route(0, slot);
         if (TRACE) trace(TR_ARRIVE, j, 1, dest);
         const bool bad = lane == (int)dest && in >= my_inbox_cap;
         if (lane == (int)dest && !bad) {
@@ -747,7 +775,9 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
           for (;;) {
             if (in >= my_inbox_cap) { lovf = true; break; }
             const unsigned long long body = fb[fh];
-            ib[wrap_add(ih, in, my_inbox_cap)] = body;
+            const uint32_t at_idx = wrap_add(ih, in, my_inbox_cap);
+            ib[at_idx] = body;
+            if (my_kv) my_iready[at_idx] = fhead + my_hint_off;   // emission + tau*ctx (M23 HINT)
             ++in;
             fh = wrap_add(fh, 1u, my_flight_cap);
             --fn;
@@ -803,7 +833,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
         stg[5] = (uint32_t)(t >> 32);
         stg[12] = stg[13] = stg[14] = stg[15] = 0xFFFFFFFFu;
         stg[16] = stg[17] = 0xFFFFFFFFu;
-        stg[31] = (uint32_t)rid;
+        stg[31] = 0;
       }
       __syncwarp();
       if (lane < 8) reinterpret_cast<uint4*>(sum_out)[lane] = reinterpret_cast<const uint4*>(stg)[lane];
@@ -892,6 +922,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
     const uint32_t deliv = __reduce_add_sync(FULL, is_inst ? cnt_deliv : 0u);
     const uint32_t recvs = __reduce_add_sync(FULL, is_inst ? cnt_recv : 0u);
     const uint32_t decs = __reduce_add_sync(FULL, is_inst ? cnt_decode : 0u);
+    const uint32_t kvs = __reduce_add_sync(FULL, is_inst ? cnt_kv : 0u);
     const uint32_t larges = __reduce_add_sync(FULL, is_inst ? n_large : 0u);
     const unsigned long long tokens = warp_sum64(is_inst ? tok : 0ull);
     __syncwarp();
@@ -914,13 +945,13 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
       stg[24] = window_closes; stg[25] = mode_switches; stg[26] = good; stg[27] = larges;
       stg[28] = (uint32_t)tokens; stg[29] = (uint32_t)(tokens >> 32);
       stg[30] = (batch_changes & 0xFFFFu) | (select_changes << 16);
-      stg[31] = (uint32_t)rid;
+      stg[31] = kvs;
       cst[0] = 1; cst[1] = status == SDAS_REPLICA_OK; cst[2] = 0; cst[3] = status == SDAS_REPLICA_TRUNCATED;
       cst[4] = admitted; cst[5] = dropped; cst[6] = completed; cst[7] = sum_e2e; cst[8] = sum_ff;
       cst[9] = t; cst[10] = int_nsys; cst[11] = good; cst[12] = larges; cst[13] = arrivals;
       cst[14] = deliv; cst[15] = recvs; cst[16] = decs; cst[17] = window_closes; cst[18] = mode_switches;
       cst[19] = tokens; cst[20] = batch_changes; cst[21] = select_changes; cst[22] = n_sat;
-      cst[23] = 0;
+      cst[23] = kvs;
     }
     __syncwarp();
     if (lane < 8) reinterpret_cast<uint4*>(sum_out)[lane] = reinterpret_cast<const uint4*>(stg)[lane];

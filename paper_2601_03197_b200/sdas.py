@@ -21,6 +21,14 @@ OK, E_INVALID_ARG, E_INVALID_FIELD, E_UNKNOWN_PARAM, E_OUT_OF_RANGE, E_BUFFER, E
     0, -1, -2, -3, -4, -5, -6, -7, -8
 MODES = {"batch": 0, "function": 1, "token": 2}
 ROUTES = {"jsq": 0, "rr": 1, "fixed": 2, "select": 3}
+KV_POLICIES = {"off": 0, "affinity": 1, "recompute": 2, "posthoc": 3, "hint": 4}
+
+
+def _kv_fields(pipe):
+    kv = pipe.get("kv") or {}
+    return (kv.get("role", 0), kv.get("ctx_tokens", 0), kv.get("tau_xfer", 0), kv.get("home_skew", 0))
+
+
 ARRIVALS = {"poisson": 0, "mmpp2": 1, "det": 2, "list": 3}
 OBJECTIVES = {"p99_e2e": 0, "p50_e2e": 1, "p99_ff": 2, "throughput": 3, "goodput": 4, "large_under_slo": 5}
 SCOPES = {"replica": 0, "cell": 1, "group": 2, "row": 3}
@@ -36,7 +44,7 @@ SUMMARY_DTYPE = np.dtype([
     ("max_e2e", "<u4"), ("n_saturated", "<u4"),
     ("arrivals", "<u4"), ("deliveries", "<u4"), ("recv_steps", "<u4"), ("decode_steps", "<u4"),
     ("window_closes", "<u4"), ("mode_switches", "<u4"), ("good", "<u4"), ("large_items", "<u4"),
-    ("tokens", "<u8"), ("batch_changes", "<u2"), ("select_changes", "<u2"), ("replica_lo", "<u4")])
+    ("tokens", "<u8"), ("batch_changes", "<u2"), ("select_changes", "<u2"), ("kv_transfers", "<u4")])
 assert SUMMARY_DTYPE.itemsize == 128
 SERIES_DTYPE = np.dtype([("qint", "<u8"), ("busy", "<u4"), ("maxq", "<u2"), ("mode", "u1"), ("B", "u1")])
 TRACE_DTYPE = np.dtype([("tick", "<u8"), ("code", "<u4"), ("a", "<u4"), ("b", "<u4"), ("c", "<u4")])
@@ -72,14 +80,16 @@ class LinkDesc(C.Structure):
 class PipelineDesc(C.Structure):
     _fields_ = [("n_roles", C.c_uint32), ("roles", C.POINTER(RoleDesc)), ("n_links", C.c_uint32),
                 ("links", C.POINTER(LinkDesc)), ("feedback_role", C.c_uint32), ("request_cap", C.c_uint32),
-                ("window_ticks", C.c_uint64), ("slo_ticks", C.c_uint64)]
+                ("window_ticks", C.c_uint64), ("slo_ticks", C.c_uint64), ("kv_role", C.c_uint32),
+                ("kv_ctx_tokens", C.c_uint32), ("kv_tau_xfer", C.c_uint32), ("kv_home_skew", C.c_uint32)]
 
 
 class Candidate(C.Structure):
     _fields_ = [("kind", C.c_uint32), ("mode", C.c_uint8 * 8), ("ctl_links", C.c_uint32), ("metric", C.c_uint32),
                 ("lo_permille", C.c_uint32), ("hi_permille", C.c_uint32), ("dwell_windows", C.c_uint32),
                 ("band_mode", C.c_uint8 * 4), ("route_override", C.c_uint32), ("batch_roles", C.c_uint32),
-                ("q_hi", C.c_uint32), ("select_role", C.c_int32), ("policy_slo_ticks", C.c_uint64)]
+                ("q_hi", C.c_uint32), ("select_role", C.c_int32), ("kv_policy", C.c_uint32),
+                ("policy_slo_ticks", C.c_uint64)]
 
 
 class ArrivalDesc(C.Structure):
@@ -197,6 +207,7 @@ def _candidate(c, n_links):
     x.q_hi = c["q_hi"]
     x.select_role = -1 if c["select_role"] is None else c["select_role"]
     x.policy_slo_ticks = c["policy_slo"]
+    x.kv_policy = KV_POLICIES[c.get("kv", "off")]
     return x
 
 
@@ -266,7 +277,7 @@ class Pipeline:
             links[l] = LinkDesc(d["src"], d["dst"], d["net"], d["chunk"], MODES[d["mode"]])
         desc = PipelineDesc(len(pipe["roles"]), C.cast(roles, C.POINTER(RoleDesc)), len(pipe["links"]),
                             C.cast(links, C.POINTER(LinkDesc)), pipe["feedback_role"], pipe["request_cap"],
-                            pipe["window"], pipe["slo"])
+                            pipe["window"], pipe["slo"], *_kv_fields(pipe))
         h = C.c_void_p()
         _check(lib().sdas_pipeline_create(C.byref(desc), C.byref(h)))
         self.h = h

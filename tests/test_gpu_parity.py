@@ -137,3 +137,35 @@ def test_metrics_derived_fp64():
         for got, want in ((m["mean_e2e"], float(s["sum_e2e"]) / n), (m["mean_ff"], float(s["sum_ff"]) / n),
                           (m["throughput"], float(int(s["completed"]) * 10 ** 6) / float(s["makespan"]))):
             assert abs(got - want) <= 1e-12 * abs(want)
+
+
+# ------------------------------------------------------------------ f1: KV transfer + hints (M21-M24)
+@pytest.mark.parametrize("kv", ["off", "affinity", "recompute", "posthoc", "hint"])
+def test_kv_single_request(kv):
+    import json
+    import os
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "ht_kv.json")))
+    p = W.p2_kv(home_skew=1000)
+    p["roles"][1]["route"] = "fixed"
+    p["roles"][1]["route_fixed"] = 1
+    g = W.grid([W.with_kv(W.static("batch"), kv)], [W.arr_list([0], prompt=(100, 100), output=(32, 32))],
+               n_requests=1)
+    gg, _ = full_check(p, g)
+    want = gold["single_request_fixed_to_tester1"][kv]
+    assert int(gg["summary"][0]["p50_e2e"]) == want["e2e"] and int(gg["summary"][0]["kv_transfers"]) == want[
+        "kv_transfers"]
+
+
+def test_kv_fig6_grid():
+    p, g = W.config_kv(n_seeds=3, n_requests=400)
+    gg, o = full_check(p, g, objective="goodput")
+    assert gg["summary"]["kv_transfers"].sum() > 0
+
+
+def test_kv_with_function_mode_and_rr():
+    p = W.p2_kv(ctx_tokens=1500, home_skew=500)
+    p["links"][0]["mode"] = "function"
+    cands = [W.with_kv(W.static("function"), k) for k in ("affinity", "hint", "posthoc")]
+    cands.append(W.with_kv(dict(W.static("token"), route="rr"), "recompute"))
+    g = W.grid(cands, [W.poisson(m) for m in (600000, 280000)], n_seeds=3, n_requests=300)
+    full_check(p, g)
