@@ -322,21 +322,17 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
       const uint32_t role = I.role;
       const DRole& R = P.role[role];
       const uint32_t bi = __shfl_sync(FULL, b, i);
-      if (lane == (int)i) {
-        st = IDLE;
-        ++cnt_decode;
-        tok += bi;
-      }
+      const bool me = lane == (int)i;
+      st = me ? IDLE : st;
+      cnt_decode += me ? 1u : 0u;
+      tok += me ? bi : 0u;
       if (TRACE) trace(TR_DECODE_DONE, i, bi, 0);
       uint32_t* const bat = at<uint32_t>(Wr, I.off_batch);
       const bool act = lane < (int)bi;
       const uint32_t n_out = R.n_out;
-      uint32_t wA = 0, wB = 0, wD = 0;
-      if (act) {
-        wA = bat[lane];
-        wB = bat[32 + lane];
-        if (MAXOUT > 1) wD = bat[96 + lane];
-      }
+      // all 32 slots are loaded (slots >= bi hold stale words that are never observed)
+      uint32_t wA = bat[lane], wB = bat[32 + lane], wD = 0;
+      if (MAXOUT > 1) wD = bat[96 + lane];
       const uint32_t slot = wA & 0xFFFu, out = wA >> 16;
       const uint32_t done = (wB & 0xFFFFu) + 1u;
       wB = (wB & 0xFFFF0000u) | done;
@@ -347,10 +343,8 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
       const uint32_t m1 = MAXOUT > 1 ? __ballot_sync(FULL, e1) : 0u;
       uint32_t wC = 0, wE = 0;
       if (m0 | m1) {
-        if (act) {
-          wC = bat[64 + lane];
-          if (MAXOUT > 1) wE = bat[128 + lane];
-        }
+        wC = bat[64 + lane];
+        if (MAXOUT > 1) wE = bat[128 + lane];
         for (int q = 0; q < MAXOUT; ++q) {
           const uint32_t mq = q ? m1 : m0;
           if (!mq) continue;
@@ -451,17 +445,15 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
         __syncwarp();
       }
       const uint32_t fin = __ballot_sync(FULL, act && done == out);
-      if (!fin) {
-        if (act) {
-          bat[32 + lane] = wB;
-          if (m0 | m1) {
-            bat[64 + lane] = wC;
-            if (MAXOUT > 1) { bat[96 + lane] = wD; bat[128 + lane] = wE; }
-          }
+      if (!fin) {  // common case: write the advanced words back in place (stale slots included)
+        bat[32 + lane] = wB;
+        if (m0 | m1) {
+          bat[64 + lane] = wC;
+          if (MAXOUT > 1) { bat[96 + lane] = wD; bat[128 + lane] = wE; }
         }
         return;
       }
-      if (lane == (int)i && my_large) n_large += __popc(fin);
+      n_large += (me && my_large) ? (uint32_t)__popc(fin) : 0u;
       uint32_t fm = fin;
       while (fm) {
         const int k = __ffs(fm) - 1;
@@ -470,7 +462,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
       }
       const bool keep = act && done != out;
       const uint32_t km = __ballot_sync(FULL, keep);
-      if (!(m0 | m1) && act) {
+      if (!(m0 | m1)) {
         wC = bat[64 + lane];
         if (MAXOUT > 1) wE = bat[128 + lane];
       }
@@ -483,7 +475,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
         if (MAXOUT > 1) { bat[96 + nk] = wD; bat[128 + nk] = wE; }
       }
       __syncwarp();
-      if (lane == (int)i) b = __popc(km);
+      b = me ? (uint32_t)__popc(km) : b;
     };
 
     // ---------------------------------------------------------------- phase START (M7)
@@ -556,19 +548,15 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
         __syncwarp();
       }
       const uint32_t nbat = bi + nadm;
-      uint32_t cost32 = 0;
-      if (lane == (int)i) {
-        wh = wrap_add(wh, nadm, my_wait_cap);
-        wn -= nadm;
-        b = nbat;
-        if (nbat > 0) {
-          unsigned long long cost = (unsigned long long)MI.tau0 + (unsigned long long)MI.gamma * nbat;
-          if (cost < 1) cost = 1;
-          cost32 = (uint32_t)cost;
-          st = DECODE;
-          end_lo = t_lo + cost32;
-        }
-      }
+      // branch-free update of instance i (tau0 < 2^31 and gamma*32 < 2^30 are validated: no u32 overflow)
+      const bool me = lane == (int)i;
+      const uint32_t cost32 = max(1u, MI.tau0 + MI.gamma * nbat);
+      wh = me ? wrap_add(wh, nadm, my_wait_cap) : wh;
+      wn = me ? wn - nadm : wn;
+      b = me ? nbat : b;
+      const bool go = me && nbat > 0;
+      st = go ? (uint32_t)DECODE : st;
+      end_lo = go ? t_lo + cost32 : end_lo;
       if (TRACE && nbat > 0) trace(TR_DECODE_START, i, nbat, __shfl_sync(FULL, cost32, i));
     };
 
@@ -714,18 +702,14 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
       __syncwarp();
       if (jn >= N && nsys == 0) break;
       // next tick: warp-min over 32-bit deltas (every pending event lies < 2^31 ticks ahead)
-      uint32_t d = 0xFFFFFFFFu;
-      if (is_inst) {
-        if (st != IDLE) d = end_lo - t_lo;
-        if (fn) d = min(d, fhead - t_lo);
-      }
-      if (lane == 0) {
-        d = min(d, nb_lo - t_lo);
-        if (arr_near) d = min(d, A_lo - t_lo);
-      }
+      // (branch-free: lanes that are not instances hold IDLE / empty state and contribute nothing)
+      uint32_t d = st != IDLE ? end_lo - t_lo : 0xFFFFFFFFu;
+      d = fn ? min(d, fhead - t_lo) : d;
+      const uint32_t d0 = min(nb_lo - t_lo, arr_near ? A_lo - t_lo : 0xFFFFFFFFu);
+      d = lane == 0 ? min(d, d0) : d;
       d = __reduce_min_sync(FULL, d);
       if (max_ticks && t + d > max_ticks) { status = SDAS_REPLICA_TRUNCATED; break; }
-      if (is_inst) {  // integrate the piecewise-constant state over [t, t + d) (M15)
+      {  // integrate the piecewise-constant state over [t, t + d) (M15)
         const uint32_t Q = in + wn;
         acc_busy += st != IDLE ? d : 0u;
         acc_qint += (unsigned long long)Q * d;
