@@ -148,7 +148,7 @@ def lib():
     global _lib
     if _lib is None:
         path = _build.LIB
-        if _build.needs_build():
+        if _build.needs_build() and "SDAS_LIB" not in os.environ:   # an explicit SDAS_LIB is never rebuilt
             _build.build()
         if not os.path.exists(path):
             raise ImportError("libsdas.so missing: run python -m paper_2601_03197_b200.build")
