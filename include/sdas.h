@@ -62,6 +62,8 @@ enum { SDAS_SCOPE_REPLICA = 0, SDAS_SCOPE_CELL = 1, SDAS_SCOPE_GROUP = 2, SDAS_S
 #define SDAS_FLAG_RECORDS 1u /* write per-request (e2e, ff) records to buffers.records */
 #define SDAS_FLAG_SERIES 2u  /* write per-window queue-length series for sampled replicas */
 #define SDAS_FLAG_TRACE 4u   /* write the event trace of grid.trace_replica (debug) */
+#define SDAS_FLAG_STEPWISE 8u /* simulate every DECODE step as its own event (no silent-run coalescing,
+                                 DESIGN.md §5); results are identical either way -- A/B and debugging */
 
 /* implementation limits (DESIGN.md §"Limits") */
 #define SDAS_MAX_ROLES 8
@@ -192,7 +194,9 @@ typedef struct {
                                 switches, 26 good, 27 large-model items, 28-29 output tokens, 30 batch|select
                                 changes (u16 pair), 31 KV transfers (M24) */
   uint64_t records_bytes;    /* device: n_local_replicas x n_requests x {u32 e2e, u32 ff} (FLAG_RECORDS) */
-  uint64_t series_bytes;     /* device: series_slots x series_windows x n_instances x 16 B (FLAG_SERIES) */
+  uint64_t series_bytes;     /* device: series_slots x series_windows x n_instances x 16 B (FLAG_SERIES);
+                                zeroed by sdas_simulate: windows a replica never reaches (it ended or
+                                overflowed first) read as 0 */
   uint64_t cell_cnt_bytes;   /* device: n_cells x SDAS_NCNT int64 (zeroed by the caller; accumulated) */
   uint64_t cell_hist_bytes;  /* device: n_cells x 2 x SDAS_NBINS int32 (zeroed by the caller) */
   uint64_t best_group_bytes; /* device: n_local_groups int32 (control_sweep) */

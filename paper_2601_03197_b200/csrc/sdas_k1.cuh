@@ -44,6 +44,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
   const uint32_t W32 = (uint32_t)P.window;
   const unsigned long long max_ticks = P.max_ticks;
   const bool need_lint = P.need_lint != 0;
+  const bool coalesce = (P.flags & SDAS_FLAG_STEPWISE) == 0;   // silent DECODE runs
   const uint32_t key0 = (uint32_t)P.master_seed, key1 = (uint32_t)(P.master_seed >> 32);
   const unsigned long long gwarp = (unsigned long long)blockIdx.x * (blockDim.x >> 5) + wib;
   unsigned long long* const rec_scratch =
@@ -108,6 +109,13 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
     int32_t qlB = -(1 << 30);
     uint32_t acc_busy = 0, acc_maxq = 0, cnt_deliv = 0, cnt_recv = 0, cnt_decode = 0, n_large = 0, cnt_kv = 0;
     uint32_t H_next = 0;   // KV home (index within kv_role) of the next arriving request (M21)
+    // A DECODE "run" is runm consecutive steps of one unchanged batch of which all but the last are
+    // silent (no emission point, no finish, no first feedback, no admission, empty inbox): they change
+    // nothing any other part of the model observes, so they complete as one event at end_lo with the
+    // per-step bookkeeping applied in bulk.  A message or arrival entering the inbox mid-run cuts the run
+    // at the first step boundary >= its tick (RECV-first START, M7); flushm > 0 = a cut landed exactly
+    // on a boundary of this tick and that many silent steps are applied before phase START.
+    uint32_t runm = 1, flushm = 0;
 
     // uniform replica state
     unsigned long long t = 0, A_next = 0, int_nsys = 0;
@@ -125,6 +133,24 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
           r->tick = t; r->code = code; r->a = a; r->b = bb; r->c = cc;
         }
       }
+    };
+    auto trace_at = [&](unsigned long long tick, uint32_t code, uint32_t a, uint32_t bb, uint32_t cc) {
+      if (TRACE && trace_on && lane == 0) {
+        const unsigned long long k = atomicAdd(reinterpret_cast<unsigned long long*>(trace_buf), 1ull);
+        if (k < P.trace_cap) {
+          TraceRec* r = reinterpret_cast<TraceRec*>(trace_buf + 8) + k;
+          r->tick = tick; r->code = code; r->a = a; r->b = bb; r->c = cc;
+        }
+      }
+    };
+    // trace records of the silent steps 1..n of a run that began at tick t_run (step length c);
+    // with_last = false: the START of step n+1 is not a DECODE start
+    auto trace_silent = [&](uint32_t i, uint32_t bi, uint32_t c, unsigned long long t_run, uint32_t n, bool last_start) {
+      if (TRACE && trace_on)
+        for (uint32_t j = 1; j <= n; ++j) {
+          trace_at(t_run + (unsigned long long)j * c, TR_DECODE_DONE, i, bi, 0);
+          if (j < n || last_start) trace_at(t_run + (unsigned long long)j * c, TR_DECODE_START, i, bi, c);
+        }
     };
     auto trace_lane = [&](uint32_t code, uint32_t a, uint32_t bb, uint32_t cc) {
       if (TRACE && trace_on) {
@@ -322,10 +348,15 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
       const uint32_t role = I.role;
       const DRole& R = P.role[role];
       const uint32_t bi = __shfl_sync(FULL, b, i);
+      const uint32_t mi = __shfl_sync(FULL, runm, i);          // steps in this run (all but the last silent)
       const bool me = lane == (int)i;
       st = me ? IDLE : st;
-      cnt_decode += me ? 1u : 0u;
-      tok += me ? bi : 0u;
+      cnt_decode += me ? mi : 0u;
+      tok += me ? (unsigned long long)mi * bi : 0ull;
+      if (TRACE && mi > 1) {
+        const uint32_t c = max(1u, I.tau0 + I.gamma * bi);
+        trace_silent(i, bi, c, t - (unsigned long long)mi * c, mi - 1u, true);
+      }
       if (TRACE) trace(TR_DECODE_DONE, i, bi, 0);
       uint32_t* const bat = at<uint32_t>(Wr, I.off_batch);
       const bool act = lane < (int)bi;
@@ -334,7 +365,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
       uint32_t wA = bat[lane], wB = bat[32 + lane], wD = 0;
       if (MAXOUT > 1) wD = bat[96 + lane];
       const uint32_t slot = wA & 0xFFFu, out = wA >> 16;
-      const uint32_t done = (wB & 0xFFFFu) + 1u;
+      const uint32_t done = (wB & 0xFFFFu) + mi;
       wB = (wB & 0xFFFF0000u) | done;
       // emission test (M9): link q emits when done reaches its next emission point
       const bool e0 = act && n_out > 0 && done == (wB >> 16);
@@ -441,6 +472,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
         }
       }
       if (role == fb_role) {  // first output token at a feedback-role instance (M13)
+        // (two items of one request may both reach done == 1 in this step: both store the same value)
         if (act && done == 1u && rFF[slot] == kUnsetFF) rFF[slot] = sat32(t - rA[slot]);
         __syncwarp();
       }
@@ -517,20 +549,22 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
       }
       if (TRACE) trace(TR_RECV_START, i, rJ[__shfl_sync(FULL, slot, i)], __shfl_sync(FULL, cost32, i));
     };
-    auto start_decode = [&](uint32_t i) {  // FIFO admission (modes bound here, M9) + DECODE step
+    auto start_decode = [&](uint32_t i) {  // FIFO admission (modes bound here, M9) + DECODE step / run
       const DInst& I = P.inst[i];
       const DRole& R = P.role[I.role];
       const uint32_t bi = __shfl_sync(FULL, b, i), Bi = __shfl_sync(FULL, Bk, i);
       const uint32_t wn_i = __shfl_sync(FULL, wn, i);
       const uint32_t nadm = Bi > bi ? min(Bi - bi, wn_i) : 0u;
+      const uint32_t n_out = R.n_out;
+      uint32_t* const bat = at<uint32_t>(Wr, I.off_batch);
+      uint32_t wA = 0, wB = 0, wD = 0;
       if (nadm) {
         const uint32_t wh_i = __shfl_sync(FULL, wh, i);
-        uint32_t* const bat = at<uint32_t>(Wr, I.off_batch);
         if (lane >= (int)bi && lane < (int)(bi + nadm)) {
           const uint32_t e = at<uint32_t>(Wr, I.off_wait)[wrap_add(wh_i, lane - bi, I.wait_cap)];
           const uint32_t out = e >> 16;
-          uint32_t wA = (e & 0xFFFu) | (out << 16), wB = 0, wD = 0;
-          for (uint32_t q = 0; q < R.n_out; ++q) {
+          wA = (e & 0xFFFu) | (out << 16);
+          for (uint32_t q = 0; q < n_out; ++q) {
             const uint32_t l = q ? R.out_link1 : R.out_link0;
             const uint32_t mode = (modes >> (2 * l)) & 3u;
             uint32_t next = out;
@@ -550,14 +584,61 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
       const uint32_t nbat = bi + nadm;
       // branch-free update of instance i (tau0 < 2^31 and gamma*32 < 2^30 are validated: no u32 overflow)
       const bool me = lane == (int)i;
-      const uint32_t cost32 = max(1u, MI.tau0 + MI.gamma * nbat);
+      const uint32_t cost32 = max(1u, I.tau0 + I.gamma * nbat);
+      // run length: steps until the first sequence reaches an emission point / its end / first feedback
+      uint32_t m = 1;
+      if (coalesce) {
+        uint32_t sk = 0xFFFFFFFFu;
+        if (lane < (int)bi) {
+          wA = bat[lane];
+          wB = bat[32 + lane];
+          if (MAXOUT > 1) wD = bat[96 + lane];
+        }
+        if (lane < (int)nbat) {
+          const uint32_t done = wB & 0xFFFFu;
+          uint32_t lim = wA >> 16;                                      // out
+          if (n_out > 0) lim = min(lim, wB >> 16);
+          if (MAXOUT > 1 && n_out > 1) lim = min(lim, wD & 0xFFFFu);
+          sk = (I.role == fb_role && done == 0u) ? 1u : lim - done;
+        }
+        m = __reduce_min_sync(FULL, sk);
+        if (m > 1) {
+          // keep every pending tick < 2^31 ahead; end at the first boundary >= the next window when the
+          // controller could change B while items wait; never step past max_ticks
+          if ((unsigned long long)m * cost32 >= (1ull << 30)) m = max(1u, (1u << 30) / cost32);
+          const uint32_t span = m * cost32;
+          if (cd.adaptive && wn_i > nadm) {
+            const uint32_t nbd = nb_lo - t_lo;
+            if (span > nbd) m = (nbd + cost32 - 1u) / cost32;
+          }
+          if (max_ticks && t + span > max_ticks)
+            m = (uint32_t)max(1ull, (max_ticks - min(t, max_ticks)) / cost32);
+        }
+      }
       wh = me ? wrap_add(wh, nadm, my_wait_cap) : wh;
       wn = me ? wn - nadm : wn;
       b = me ? nbat : b;
       const bool go = me && nbat > 0;
       st = go ? (uint32_t)DECODE : st;
-      end_lo = go ? t_lo + cost32 : end_lo;
-      if (TRACE && nbat > 0) trace(TR_DECODE_START, i, nbat, __shfl_sync(FULL, cost32, i));
+      end_lo = go ? t_lo + m * cost32 : end_lo;
+      runm = go ? m : runm;
+      if (TRACE && nbat > 0) trace(TR_DECODE_START, i, nbat, cost32);
+    };
+    // lane-local: a message / arrival enters this instance's inbox at tick t while it may be mid-run
+    auto cut_run = [&]() {
+      if (st != DECODE || runm <= 1u) return;
+      const uint32_t c = max(1u, MI.tau0 + MI.gamma * b);
+      const uint32_t rs = end_lo - runm * c;                 // run start (>= 1 tick ago)
+      const uint32_t mp = (t_lo - rs + c - 1u) / c;          // first boundary >= t
+      if (mp >= runm) return;
+      if (rs + mp * c != t_lo) {
+        runm = mp;
+        end_lo = rs + mp * c;
+      } else {                                               // boundary at this very tick: flush it
+        flushm = mp;
+        runm = mp;
+        end_lo = t_lo;
+      }
     };
 
     // ---------------------------------------------------------------- phase ARRIVE (M14)
@@ -576,6 +657,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
         const uint32_t word = __shfl_sync(FULL, wv, wi);
         const uint32_t bit = __ffs(word) - 1;
         const uint32_t slot = (uint32_t)wi * 32u + bit;
+        __syncwarp();                     // every lane's bitmap read precedes lane 0's update
         if (lane == 0) {
           bitmap[wi] = word & ~(1u << bit);
           rA[slot] = t;
@@ -593,6 +675,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
           reinterpret_cast<unsigned long long*>(my_inbox)[wrap_add(ih, in, my_inbox_cap)] =
               make_body(slot, F_OPENS | F_CLOSES, P_next, P_next);
           ++in;
+          if (coalesce) cut_run();
         }
         if (__ballot_sync(FULL, bad)) {
           if (TRACE) trace(TR_OVERFLOW, 0, dest, 0);
@@ -742,6 +825,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
           else complete_decode((uint32_t)i);
           if (ovf) break;
           if ((early >> i) & 1u) {
+            __syncwarp();                  // the wait-ring entry lane 0 just pushed (complete_recv)
             const uint32_t busy_i = __ballot_sync(FULL, (st != IDLE || in != 0u) && lane == i);
             if (!busy_i) start_decode((uint32_t)i);
           }
@@ -753,6 +837,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
       if (__ballot_sync(FULL, dv)) {
         bool lovf = false;
         if (dv) {
+          if (coalesce) cut_run();
           const uint32_t* ft = reinterpret_cast<const uint32_t*>(my_ftick);
           const unsigned long long* fb = reinterpret_cast<const unsigned long long*>(my_fbody);
           unsigned long long* ib = reinterpret_cast<unsigned long long*>(my_inbox);
@@ -785,6 +870,27 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
           arrive();
         } while (!ovf && jn < N && arr_near && A_lo == t_lo);
         if (ovf) break;
+      }
+      // runs cut exactly at this tick: apply their silent steps (they precede START, as in M12)
+      if (coalesce) {
+        uint32_t fm = __ballot_sync(FULL, flushm != 0u);
+        while (fm) {
+          const int i = __ffs(fm) - 1;
+          fm &= fm - 1;
+          const uint32_t n = __shfl_sync(FULL, flushm, i), bi = __shfl_sync(FULL, b, i);
+          uint32_t* const bat = at<uint32_t>(Wr, P.inst[i].off_batch);
+          if (lane < (int)bi) bat[32 + lane] += n;        // done += n (stays below every stop point)
+          if (lane == i) {
+            st = IDLE;
+            cnt_decode += n;
+            tok += (unsigned long long)n * b;
+            flushm = 0;
+          }
+          if (TRACE) {
+            const uint32_t c = max(1u, P.inst[i].tau0 + P.inst[i].gamma * bi);
+            trace_silent(i, bi, c, t - (unsigned long long)n * c, n, false);
+          }
+        }
       }
       // phase 4 START (idle instances with work, increasing index)
       __syncwarp();                        // wait-ring / request-table writes of this tick are visible

@@ -307,6 +307,10 @@ int launch_simulate(const uint8_t* params_dev, const DParams& hp, const sdas_buf
   if (e != cudaSuccess) return (int)e;
   e = cudaMemsetAsync(bf->work, 0, sizeof(Work), s);
   if (e != cudaSuccess) return (int)e;
+  if ((hp.flags & SDAS_FLAG_SERIES) && bf->series && hp.series_stride) {   // windows never reached read 0
+    e = cudaMemsetAsync(bf->series, 0, (size_t)hp.series_slots * hp.series_windows * hp.n_inst * 16u, s);
+    if (e != cudaSuccess) return (int)e;
+  }
   if ((hp.flags & SDAS_FLAG_TRACE) && bf->trace) {
     e = cudaMemsetAsync(bf->trace, 0, 8, s);
     if (e != cudaSuccess) return (int)e;

@@ -32,7 +32,7 @@ def _kv_fields(pipe):
 ARRIVALS = {"poisson": 0, "mmpp2": 1, "det": 2, "list": 3}
 OBJECTIVES = {"p99_e2e": 0, "p50_e2e": 1, "p99_ff": 2, "throughput": 3, "goodput": 4, "large_under_slo": 5}
 SCOPES = {"replica": 0, "cell": 1, "group": 2, "row": 3}
-FLAG_RECORDS, FLAG_SERIES, FLAG_TRACE = 1, 2, 4
+FLAG_RECORDS, FLAG_SERIES, FLAG_TRACE, FLAG_STEPWISE = 1, 2, 4, 8
 NBINS, NCNT = 464, 24
 ROUTE_NONE = 255
 

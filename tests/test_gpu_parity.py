@@ -169,3 +169,34 @@ def test_kv_with_function_mode_and_rr():
     cands.append(W.with_kv(dict(W.static("token"), route="rr"), "recompute"))
     g = W.grid(cands, [W.poisson(m) for m in (600000, 280000)], n_seeds=3, n_requests=300)
     full_check(p, g)
+
+
+# ------------------------------------------------------------------ silent-run coalescing
+@pytest.mark.parametrize("cfg", ["config1", "config2", "config3", "config4", "kv", "trunc"])
+def test_coalesced_runs_equal_stepwise(cfg):
+    """SDAS_FLAG_STEPWISE (one event per DECODE step) and the default coalesced runs give identical bytes:
+    summaries, records, series and cells."""
+    if cfg == "config1":
+        p, g = W.config1(n_seeds=3, n_requests=800)
+    elif cfg == "config2":
+        p, g = W.config2(n_seeds=3, n_requests=400, series_stride=5, series_windows=64)
+    elif cfg == "config3":
+        p, g = W.config3(n_seeds=2, n_requests=250)
+    elif cfg == "config4":
+        p, g = W.config4(n_seeds=1, n_requests=300, candidates=W.config4_candidates()[::97])
+    elif cfg == "kv":
+        p, g = W.config_kv(n_seeds=3, n_requests=300)
+    else:
+        p = W.p2_x()
+        cands = [W.adaptive(["function"], metric="load", lo=2000, hi=6000), W.static("batch"), W.static("token")]
+        g = W.grid(cands, [W.poisson(m) for m in (998500, 399400)], n_seeds=3, n_requests=600,
+                   max_ticks=150_000_000)
+    series = g.get("series_stride", 0) > 0
+    a = run_gpu(p, g, series=series)
+    b = run_gpu(p, g, series=series, stepwise=True)
+    assert a["summary"].tobytes() == b["summary"].tobytes()
+    for x, n in enumerate(a["summary"]["completed"]):   # records past `completed` are never written
+        assert np.array_equal(a["records"][x, :n], b["records"][x, :n])
+    assert np.array_equal(a["cells"][0], b["cells"][0]) and np.array_equal(a["cells"][1], b["cells"][1])
+    if series:
+        assert a["series"].tobytes() == b["series"].tobytes()
