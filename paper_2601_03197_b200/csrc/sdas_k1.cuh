@@ -813,22 +813,12 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
       uint32_t cm = __ballot_sync(FULL, done_here);
       if (cm) {
         const uint32_t rm = __ballot_sync(FULL, done_here && st == RECV);
-        // An instance whose inbox stays empty and that receives no delivery / arrival at this tick
-        // takes the same START decision now as in phase 4 (START is invariant for JSQ loads, and
-        // modes / B change only at phase 0), so its next DECODE step is started right away.
-        const uint32_t early = __ballot_sync(FULL, done_here && !(fn > 0 && fhead == t_lo) &&
-                                                       !(my_role == 0 && arr_near && A_lo == t_lo));
         do {
           const int i = __ffs(cm) - 1;
           cm &= cm - 1;
           if ((rm >> i) & 1u) complete_recv((uint32_t)i);
           else complete_decode((uint32_t)i);
           if (ovf) break;
-          if ((early >> i) & 1u) {
-            __syncwarp();                  // the wait-ring entry lane 0 just pushed (complete_recv)
-            const uint32_t busy_i = __ballot_sync(FULL, (st != IDLE || in != 0u) && lane == i);
-            if (!busy_i) start_decode((uint32_t)i);
-          }
         } while (cm);
         if (ovf) break;
       }
