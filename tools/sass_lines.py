@@ -1,5 +1,7 @@
 """Aggregate ncu per-SASS-instruction counts by CUDA source line (needs -lineinfo builds).
-usage: python tools/sass_lines.py <report.ncu-rep> <libsdas.so> <kernel-substr> [top]"""
+usage: python tools/sass_lines.py <report.ncu-rep> <libsdas.so> <kernel-substr> [top]
+env: COL=<source-page column> ranks lines by that column (e.g. stall_no_inst); REV=<git rev> reads the
+source text from that revision (when the profiled build is older than the tree)."""
 import csv, io, os, re, subprocess, sys, tempfile, collections
 rep, so, kname = sys.argv[1], sys.argv[2], sys.argv[3]
 top = int(sys.argv[4]) if len(sys.argv) > 4 else 40
@@ -26,7 +28,7 @@ out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-so
 rows = list(csv.reader(io.StringIO(out)))
 hdr = rows[1]
 ia, ie = hdr.index("Address"), hdr.index("Instructions Executed")
-isamp = hdr.index("# Samples") if "# Samples" in hdr else None
+isamp = hdr.index(os.environ["COL"]) if os.environ.get("COL") else (hdr.index("# Samples") if "# Samples" in hdr else None)
 agg, samp, tot = collections.Counter(), collections.Counter(), 0
 base = None
 for r in rows[2:]:
@@ -50,9 +52,16 @@ src = {}
 for (f, l) in agg:
     if f not in src:
         p = os.path.join(os.path.dirname(os.path.abspath(so)), "csrc", f)
-        src[f] = open(p).read().splitlines() if os.path.exists(p) else []
-print("total warp instructions %.4g" % tot)
-for (f, l), n in agg.most_common(top):
+        if os.environ.get("REV") and os.path.exists(p):
+            rel = os.path.relpath(p, subprocess.run(["git", "rev-parse", "--show-toplevel"], capture_output=True,
+                                                    text=True).stdout.strip())
+            src[f] = subprocess.run(["git", "show", "%s:%s" % (os.environ["REV"], rel)], capture_output=True,
+                                    text=True).stdout.splitlines()
+        else:
+            src[f] = open(p).read().splitlines() if os.path.exists(p) else []
+print("total warp instructions %.4g; column %s total %.4g" % (tot, os.environ.get("COL", "# Samples"), sum(samp.values())))
+for (f, l), n in (samp if os.environ.get("COL") else agg).most_common(top):
+    n = agg[(f, l)]
     s = src.get(f, [])
     txt = s[l - 1].strip()[:90] if 0 < l <= len(s) else ""
     print("%6.2f%% %8.3g  smp %7d  %s:%d  %s" % (100 * n / tot, n, samp[(f, l)], f, l, txt))
