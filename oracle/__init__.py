@@ -48,7 +48,8 @@ def _kv(pipe):
     return (kv.get("role", 0), kv.get("ctx_tokens", 0), kv.get("tau_xfer", 0), kv.get("home_skew", 0))
 ROUTES = {"jsq": 0, "rr": 1, "fixed": 2, "select": 3}
 ARRIVALS = {"poisson": 0, "mmpp2": 1, "det": 2, "list": 3}
-OBJECTIVES = {"p99_e2e": 0, "p50_e2e": 1, "p99_ff": 2, "throughput": 3, "goodput": 4, "large_under_slo": 5}
+OBJECTIVES = {"p99_e2e": 0, "p50_e2e": 1, "p99_ff": 2, "throughput": 3, "goodput": 4, "large_under_slo": 5,
+              "p90_e2e": 6}
 STATUS = {0: "ok", 1: "overflow", 2: "truncated"}
 CELL_FIELDS = ["n_replicas", "n_ok", "n_overflow", "n_truncated", "admitted", "dropped", "completed",
                "sum_e2e", "sum_ff", "makespan_sum", "int_nsys", "good", "large_items", "arrivals",
@@ -91,7 +92,7 @@ class Candidate(C.Structure):
                 ("metric_load", C.c_uint32), ("lo", C.c_uint32), ("hi", C.c_uint32), ("dwell", C.c_uint32),
                 ("band", C.c_uint32 * 3), ("route_override", C.c_uint32), ("batch_roles", C.c_uint32),
                 ("q_hi", C.c_uint32), ("select_role", C.c_int32), ("policy_slo", C.c_uint64),
-                ("kv_policy", C.c_uint32)]
+                ("kv_policy", C.c_uint32), ("guard_links", C.c_uint32), ("guard_pct", C.c_uint32)]
 
 
 class Pipeline(C.Structure):
@@ -118,7 +119,7 @@ SUMMARY_FIELDS = [
     ("arrivals", np.uint32), ("deliveries", np.uint32), ("recv_steps", np.uint32), ("decode_steps", np.uint32),
     ("window_closes", np.uint32), ("mode_switches", np.uint32), ("good", np.uint32), ("large_items", np.uint32),
     ("tokens", np.uint64), ("stop_tick", np.uint64), ("replica", np.uint64),
-    ("batch_changes", np.uint32), ("select_changes", np.uint32), ("kv_transfers", np.uint32), ("pad_kv", np.uint32),
+    ("batch_changes", np.uint32), ("select_changes", np.uint32), ("kv_transfers", np.uint32), ("p90_e2e", np.uint32),
     ("msgs_emitted", np.uint64), ("tokens_emitted", np.uint64), ("msgs_received", np.uint64),
     ("tokens_received", np.uint64),
 ]
@@ -204,6 +205,8 @@ def _candidate(c, n_links):
     x.select_role = -1 if c["select_role"] is None else c["select_role"]
     x.policy_slo = c["policy_slo"]
     x.kv_policy = KV_POLICIES[c.get("kv", "off")]
+    x.guard_links = sum(1 << l for l in c.get("guard_links", ()))
+    x.guard_pct = c.get("guard_pct", 90)
     return x
 
 

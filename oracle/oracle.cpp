@@ -265,6 +265,7 @@ struct Replica {
   std::vector<std::vector<uint32_t>> out_links;    // per role, links in index order
   std::vector<int32_t> in_link;                    // per role
   std::vector<uint32_t> cur_mode;                  // per link (controller state)
+  std::vector<uint32_t> base_mode;                 // per link: the candidate's initial mode (M25 reset)
   std::vector<int64_t> q_last_mode;
   std::vector<uint32_t> rr;                        // per role
   std::vector<uint32_t> sel;                       // per role
@@ -548,17 +549,35 @@ struct Replica {
 
   void control(int64_t q) {  // M16, at the close of window q-1
     const uint64_t W = P.window;
-    // (i) three-band mode policy per controlled link
+    // (i) three-band mode policy per controlled link, and M25 (f3, compiled intents): a guarded link
+    // is set to BATCH while fewer than ceil(guard_pct * n / 100) of the window's n >= 1 completions
+    // met policy_slo (its guard_pct-quantile violates the bound), and otherwise reset to its initial
+    // mode -- unless the band policy drives it, which then decides.  One decision per link per window,
+    // with the same dwell / no-op suppression.
+    bool gviol = false;
+    if (cand.guard_links && w_n >= 1) gviol = w_good < (uint32_t)(((uint64_t)cand.guard_pct * w_n + 99) / 100);
     for (uint32_t l = 0; l < P.n_links; ++l) {
-      if (!((cand.ctl_links >> l) & 1)) continue;
-      uint32_t d = P.links[l].dst;
-      uint64_t u = 0;
-      for (uint32_t x = 0; x < role_n[d]; ++x) {
-        const Inst& I = inst[role_first[d] + x];
-        u += cand.metric_load ? I.w_lint : I.w_busy;
+      const bool ctl = (cand.ctl_links >> l) & 1, grd = (cand.guard_links >> l) & 1;
+      if (!ctl && !grd) continue;
+      uint32_t nm;
+      if (grd && gviol) {
+        nm = cur_mode[l];
+        if (nm != ORC_BATCH && q - q_last_mode[l] >= (int64_t)cand.dwell) { nm = ORC_BATCH; q_last_mode[l] = q; }
+      } else if (ctl) {
+        uint32_t d = P.links[l].dst;
+        uint64_t u = 0;
+        for (uint32_t x = 0; x < role_n[d]; ++x) {
+          const Inst& I = inst[role_first[d] + x];
+          u += cand.metric_load ? I.w_lint : I.w_busy;
+        }
+        nm = mode_step(u, cand.lo, cand.hi, W, role_n[d], cand.band, cand.dwell, q, cur_mode[l], &q_last_mode[l]);
+      } else {
+        nm = cur_mode[l];
+        if (w_n >= 1 && nm != base_mode[l] && q - q_last_mode[l] >= (int64_t)cand.dwell) {
+          nm = base_mode[l];
+          q_last_mode[l] = q;
+        }
       }
-      uint32_t nm = mode_step(u, cand.lo, cand.hi, W, role_n[d], cand.band, cand.dwell, q, cur_mode[l],
-                              &q_last_mode[l]);
       if (nm != cur_mode[l]) {
         cur_mode[l] = nm;
         S.mode_switches++;
@@ -647,6 +666,7 @@ struct Replica {
     q_last_mode.assign(P.n_links, INT64_MIN / 2);
     for (uint32_t l = 0; l < P.n_links; ++l)
       cur_mode[l] = cand.mode[l] == 255 ? P.links[l].mode : cand.mode[l];
+    base_mode = cur_mode;
     rr.assign(P.n_roles, 0);
     sel.resize(P.n_roles);
     for (uint32_t r = 0; r < P.n_roles; ++r) {
@@ -728,6 +748,7 @@ struct Replica {
       std::memset(hist, 0, sizeof(uint32_t) * 2 * ORC_NBINS);
       S.p50_e2e = S.p99_e2e = S.p50_ff = S.p99_ff = 0xFFFFFFFFu;
       S.bin_p50_e2e = S.bin_p99_e2e = S.bin_p50_ff = S.bin_p99_ff = 0xFFFFu;
+      S.p90_e2e = 0xFFFFFFFFu;
       return 0;
     }
     // final partial window: series only
@@ -753,6 +774,8 @@ struct Replica {
     };
     pct(ve, hist, 50, S.p50_e2e, S.bin_p50_e2e);
     pct(ve, hist, 99, S.p99_e2e, S.bin_p99_e2e);
+    uint32_t bin90;
+    pct(ve, hist, 90, S.p90_e2e, bin90);
     pct(vf, hist + ORC_NBINS, 50, S.p50_ff, S.bin_p50_ff);
     pct(vf, hist + ORC_NBINS, 99, S.p99_ff, S.bin_p99_ff);
     return 0;
@@ -939,7 +962,8 @@ void orc_argmin_groups(const orc_grid* g, const orc_summary* sums, uint32_t obj,
       Key k{};
       k.bad = x.status != ORC_OK;
       k.dropped = x.dropped;
-      k.p = obj == ORC_OBJ_P50_E2E ? x.p50_e2e : obj == ORC_OBJ_P99_FF ? x.p99_ff : x.p99_e2e;
+      k.p = obj == ORC_OBJ_P50_E2E ? x.p50_e2e : obj == ORC_OBJ_P99_FF ? x.p99_ff
+          : obj == ORC_OBJ_P90_E2E ? x.p90_e2e : x.p99_e2e;
       k.sum = obj == ORC_OBJ_P99_FF ? x.sum_ff : x.sum_e2e;
       k.completed = x.completed; k.makespan = x.makespan; k.good = x.good; k.large = x.large_items;
       k.c = (uint32_t)c;
@@ -964,7 +988,7 @@ void orc_argmin_rows(const orc_grid* g, const int64_t* cnt, const int64_t* hist,
       for (int b = 0; b < ORC_NBINS; ++b) n += (uint64_t)h[b];
       uint64_t p = 0xFFFFFFFFull;
       if (n > 0) {
-        uint32_t num = obj == ORC_OBJ_P50_E2E ? 50 : 99;
+        uint32_t num = obj == ORC_OBJ_P50_E2E ? 50 : obj == ORC_OBJ_P90_E2E ? 90 : 99;
         uint64_t k = (num * n + 99) / 100, cum = 0;
         for (uint32_t b = 0; b < ORC_NBINS; ++b) {
           cum += (uint64_t)h[b];

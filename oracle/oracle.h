@@ -23,7 +23,7 @@ enum { ORC_POISSON = 0, ORC_MMPP2 = 1, ORC_DET = 2, ORC_LIST = 3 };
 enum { ORC_OK = 0, ORC_OVERFLOW = 1, ORC_TRUNCATED = 2 };
 enum { ORC_KV_OFF = 0, ORC_KV_AFFINITY = 1, ORC_KV_RECOMPUTE = 2, ORC_KV_POSTHOC = 3, ORC_KV_HINT = 4 };
 enum { ORC_OBJ_P99_E2E = 0, ORC_OBJ_P50_E2E = 1, ORC_OBJ_P99_FF = 2, ORC_OBJ_THROUGHPUT = 3,
-       ORC_OBJ_GOODPUT = 4, ORC_OBJ_LARGE_UNDER_SLO = 5 };
+       ORC_OBJ_GOODPUT = 4, ORC_OBJ_LARGE_UNDER_SLO = 5, ORC_OBJ_P90_E2E = 6 };
 
 #define ORC_NBINS 464
 #define ORC_MAX_LINKS 8
@@ -64,6 +64,8 @@ typedef struct {
   int32_t select_role;            /* -1 none */
   uint64_t policy_slo;
   uint32_t kv_policy;             /* ORC_KV_* (rules M21-M24) */
+  uint32_t guard_links;           /* M25 (f3): links flipped to BATCH while the window e2e quantile */
+  uint32_t guard_pct;             /*   guard_pct (e.g. 90) exceeds policy_slo; else reset to base  */
 } orc_candidate;
 
 typedef struct {
@@ -94,7 +96,7 @@ typedef struct {
   uint64_t tokens;
   uint64_t stop_tick;
   uint64_t replica;
-  uint32_t batch_changes, select_changes, kv_transfers, pad_kv;
+  uint32_t batch_changes, select_changes, kv_transfers, p90_e2e;   /* p90_e2e: exact nearest rank (f3) */
   uint64_t msgs_emitted, tokens_emitted;     /* conservation checks */
   uint64_t msgs_received, tokens_received;
 } orc_summary;
