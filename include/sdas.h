@@ -56,7 +56,8 @@ enum { SDAS_KV_OFF = 0, SDAS_KV_AFFINITY = 1, SDAS_KV_RECOMPUTE = 2, SDAS_KV_POS
 enum { SDAS_METRIC_BUSY = 0, SDAS_METRIC_LOAD = 1 };
 enum { SDAS_REPLICA_OK = 0, SDAS_REPLICA_OVERFLOW = 1, SDAS_REPLICA_TRUNCATED = 2 };
 enum { SDAS_MIN_P99_E2E = 0, SDAS_MIN_P50_E2E = 1, SDAS_MIN_P99_FF = 2, SDAS_MAX_THROUGHPUT = 3,
-       SDAS_MAX_GOODPUT = 4, SDAS_MAX_LARGE_FRAC_UNDER_SLO = 5 };          /* rule M20 */
+       SDAS_MAX_GOODPUT = 4, SDAS_MAX_LARGE_FRAC_UNDER_SLO = 5,
+       SDAS_MIN_P90_E2E = 6 };                                               /* rule M20 (+ f3 p90) */
 enum { SDAS_SCOPE_REPLICA = 0, SDAS_SCOPE_CELL = 1, SDAS_SCOPE_GROUP = 2, SDAS_SCOPE_ROW = 3 };
 
 #define SDAS_FLAG_RECORDS 1u /* write per-request (e2e, ff) records to buffers.records */
@@ -155,6 +156,10 @@ typedef struct {
   uint32_t q_hi;              /* M16(ii): grow B when the window's integral Q > q_hi * W */
   int32_t select_role;        /* -1, or the SELECT role driven by model selection (M16(iii)) */
   uint32_t kv_policy;         /* SDAS_KV_*: routing / KV handling into kv_role (M21-M24) */
+  uint32_t guard_links;       /* M25 constraint guard (f3): links set to BATCH while fewer than
+                                 ceil(guard_pct * n / 100) of a window's n >= 1 completions met
+                                 policy_slo_ticks, else reset to their initial mode (needs ADAPTIVE) */
+  uint32_t guard_pct;         /* 0..100: the guarded end-to-end quantile (90 = p90) */
   uint64_t policy_slo_ticks;  /* SLO used by the controller's window p99 test */
 } sdas_candidate;
 
@@ -189,7 +194,7 @@ typedef struct {
   uint64_t summary_bytes;    /* device: n_local_replicas x 128-byte summary records, little-endian u32 words:
                                 0 status, 1 admitted, 2 dropped, 3 completed, 4-5 makespan (or overflow tick),
                                 6-7 sum e2e, 8-9 sum ff, 10-11 integral N_sys dt, 12-15 p50/p99 e2e, p50/p99 ff,
-                                16-17 their bins (u16 pairs), 18 max e2e, 19 saturated records, 20 arrivals,
+                                16 bins of p50/p99 e2e (u16 pair), 17 exact p90 e2e (f3), 18 max e2e, 19 saturated records, 20 arrivals,
                                 21 deliveries, 22 RECV steps, 23 DECODE steps, 24 window closes, 25 mode
                                 switches, 26 good, 27 large-model items, 28-29 output tokens, 30 batch|select
                                 changes (u16 pair), 31 KV transfers (M24) */
@@ -240,6 +245,7 @@ typedef struct {
   uint64_t n_replicas, admitted, dropped, completed;
   uint32_t p50_e2e, p99_e2e, p50_ff, p99_ff;      /* exact (REPLICA) or bin lower edge (CELL/ROW) */
   uint32_t bin_p50_e2e, bin_p99_e2e, bin_p50_ff, bin_p99_ff;
+  uint32_t p90_e2e, pad0;                         /* exact (REPLICA) or bin lower edge (CELL) p90 e2e */
   double mean_e2e, mean_ff;                       /* (double)sum / (double)n  (M19) */
   double throughput, goodput;                     /* completed*1e6/makespan, good*1e6/makespan (req/s) */
   uint64_t makespan, sum_e2e, sum_ff, int_nsys, good, large_items;
@@ -249,6 +255,40 @@ typedef struct {
   const uint8_t* series;                          /* REPLICA scope with FLAG_SERIES: 16 B records */
   uint64_t series_len;                            /* windows x instances */
 } sdas_metrics_out;
+
+/* ---- f3: intent compilation ("declarative ... goals", 188 "compile these into concrete
+ * policy rules", 220 intent-driven control; SPEC.md:432-436 Intent, 475-483 compile_intent) ----
+ * An intent is an objective and/or explicit rules plus latency constraints.  It compiles, on the host,
+ * into one M16/M25 policy vector (sdas_candidate) -- the unit the sweep evaluates -- and the M20
+ * objective its sweep should rank by.  Templates (DESIGN.md §2 M25 and readings):
+ *   MAX_THROUGHPUT : ADAPTIVE three-band comm_mode on every link, BUSY metric of the destination,
+ *                    lo 400 / hi 800 permille, bands TOKEN / FUNCTION / BATCH, dwell = ceil(1 s / W)
+ *                    windows; objective SDAS_MAX_THROUGHPUT.
+ *   MIN_P90_LATENCY: TOKEN on every link (chunk = the link's chunk_tokens knob); objective
+ *                    SDAS_MIN_P90_E2E.
+ *   each constraint: a guard (M25) on its scope links with guard_pct = its quantile and
+ *                    policy_slo_ticks = its bound; makes the policy ADAPTIVE.
+ *   rules          : an explicit policy vector, passed through unchanged; an objective template then
+ *                    overwrites only the mode fields (modes, kind, ctl_links, metric, lo/hi, bands,
+ *                    dwell); with no objective the sweep objective is SDAS_MIN_P99_E2E.
+ * Errors: SDAS_E_INVALID_ARG (NULL, bad enum, or InvalidIntent: no objective and no rules),
+ * SDAS_E_LIMIT (constraints with different (metric, bound), or a bound that conflicts with the rules'
+ * own policy_slo_ticks: one latency bound per compiled policy). */
+enum { SDAS_INTENT_NONE = 0, SDAS_INTENT_MAX_THROUGHPUT = 1, SDAS_INTENT_MIN_P90_LATENCY = 2 };
+enum { SDAS_CONSTRAINT_E2E_P90 = 0, SDAS_CONSTRAINT_E2E_P99 = 1 };
+typedef struct {
+  uint32_t metric;            /* SDAS_CONSTRAINT_*: a window quantile of end-to-end latency */
+  uint32_t scope_links;       /* bitmask of links flipped to BATCH while violated; 0 = every link */
+  uint64_t bound_ticks;       /* constraint: metric <= bound */
+} sdas_constraint;
+typedef struct {
+  uint32_t objective;                         /* SDAS_INTENT_* */
+  uint32_t n_constraints;
+  const sdas_constraint* constraints;
+  const sdas_candidate* rules;                /* optional explicit policy vector (NULL = none) */
+} sdas_intent;
+sdas_status sdas_compile_intent(const sdas_pipeline* p, const sdas_intent* intent, sdas_candidate* out,
+                                uint32_t* objective_out);
 
 /* host: host copies of the device buffers (only those the scope needs, same layout).
  * REPLICA: index = local replica; CELL: index = cell (i*K + k)*C + c; GROUP: local group;

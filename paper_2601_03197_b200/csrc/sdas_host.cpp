@@ -70,6 +70,13 @@ struct sdas_pipeline {
 
 namespace {
 
+uint32_t host_bin(uint32_t v) {   // rule M17 bin of an exact percentile (0xFFFF when there is none)
+  if (v == 0xFFFFFFFFu) return 0xFFFFu;
+  if (v < 16u) return v;
+  uint32_t e = 31u - (uint32_t)__builtin_clz(v);
+  return 16u + 16u * (e - 4u) + ((v >> (e - 4u)) & 15u);
+}
+
 sdas_status validate_desc(const sdas_pipeline_desc* d) {
   if (!d) return fail(SDAS_E_INVALID_ARG, "desc is NULL");
   if (d->n_roles == 0 || !d->roles) return fail(SDAS_E_INVALID_FIELD, "n_roles: at least one role required");
@@ -281,7 +288,11 @@ sdas_status plan(const sdas_pipeline* p, const sdas_grid* g, Plan& pl) {
   h.kv_tau = p->kv_tau;
   h.kv_skew32 = ((uint64_t)p->kv_skew << 32) / 1000;
   for (uint32_t cc = 0; cc < g->n_candidates; ++cc)
+  {
     if (g->cand[cc].kv_policy > SDAS_KV_HINT) return fail(SDAS_E_INVALID_FIELD, "cand[%u].kv_policy: bad enum", cc);
+    if (g->cand[cc].guard_pct > 100) return fail(SDAS_E_INVALID_FIELD, "cand[%u].guard_pct > 100", cc);
+    if (g->cand[cc].guard_links >> nl) return fail(SDAS_E_INVALID_FIELD, "cand[%u].guard_links: no such link", cc);
+  }
   h.need_lint = 0;
   for (uint32_t cc = 0; cc < g->n_candidates; ++cc)
     if (g->cand[cc].kind == SDAS_ADAPTIVE && g->cand[cc].metric == SDAS_METRIC_LOAD) h.need_lint = 1;
@@ -377,7 +388,9 @@ void pack_blob(const sdas_grid* g, const Plan& pl, std::vector<uint8_t>& blob) {
     for (int k = 0; k < 4; ++k) d.band[k] = s.band_mode[k];
     d.route_override = s.route_override; d.batch_roles = s.batch_roles; d.q_hi = s.q_hi;
     d.select_role = s.select_role; d.policy_slo = s.policy_slo_ticks;
-    d.kv_policy = s.kv_policy;
+    d.kv_policy = (uint8_t)s.kv_policy;
+    d.guard_links = (uint8_t)s.guard_links;
+    d.guard_pct = (uint8_t)s.guard_pct;
   }
   const uint64_t nIK = (uint64_t)g->n_rates * g->n_profiles;
   DArr* da = reinterpret_cast<DArr*>(blob.data() + pl.hp.off_arr);
@@ -550,7 +563,7 @@ sdas_status sdas_simulate(const sdas_pipeline* p, const sdas_grid* grid, const s
 
 sdas_status sdas_control_sweep(const sdas_pipeline* p, const sdas_grid* grid, uint32_t objective,
                                uint64_t objective_slo, const sdas_buffers* dev, void* stream) {
-  if (objective > SDAS_MAX_LARGE_FRAC_UNDER_SLO) return fail(SDAS_E_INVALID_ARG, "objective: bad enum");
+  if (objective > SDAS_MIN_P90_E2E) return fail(SDAS_E_INVALID_ARG, "objective: bad enum");
   if (dev && !dev->best_group) return fail(SDAS_E_BUFFER, "control_sweep needs best_group");
   Plan pl;
   sdas_status s = run_sim(p, grid, dev, stream, pl);
@@ -563,7 +576,7 @@ sdas_status sdas_control_sweep(const sdas_pipeline* p, const sdas_grid* grid, ui
 
 sdas_status sdas_group_argmin(const sdas_pipeline* p, const sdas_grid* grid, uint32_t objective,
                               uint64_t objective_slo, const sdas_buffers* dev, void* stream) {
-  if (objective > SDAS_MAX_LARGE_FRAC_UNDER_SLO) return fail(SDAS_E_INVALID_ARG, "objective: bad enum");
+  if (objective > SDAS_MIN_P90_E2E) return fail(SDAS_E_INVALID_ARG, "objective: bad enum");
   if (!dev || !dev->params || !dev->summary || !dev->best_group)
     return fail(SDAS_E_BUFFER, "group_argmin needs params, summary and best_group");
   Plan pl;
@@ -582,7 +595,7 @@ sdas_status sdas_group_argmin(const sdas_pipeline* p, const sdas_grid* grid, uin
 
 sdas_status sdas_finalize(const sdas_pipeline* p, const sdas_grid* grid, uint32_t objective, uint64_t objective_slo,
                           const sdas_buffers* dev, void* stream) {
-  if (objective > SDAS_MAX_LARGE_FRAC_UNDER_SLO) return fail(SDAS_E_INVALID_ARG, "objective: bad enum");
+  if (objective > SDAS_MIN_P90_E2E) return fail(SDAS_E_INVALID_ARG, "objective: bad enum");
   if (!dev || !dev->params || !dev->work || !dev->cell_cnt || !dev->cell_hist || !dev->best_row)
     return fail(SDAS_E_BUFFER, "finalize needs params, work, cell_cnt, cell_hist and best_row");
   Plan pl;
@@ -596,6 +609,68 @@ sdas_status sdas_finalize(const sdas_pipeline* p, const sdas_grid* grid, uint32_
   int rc = launch_finalize(reinterpret_cast<const uint8_t*>(dev->params), pl.hp, dev, objective, objective_slo,
                            pl.n_cells, pl.n_rows, stream);
   if (rc) return fail(SDAS_E_CUDA, "K4/K5 launch: %s", cuda_error_string(rc));
+  return ok();
+}
+
+sdas_status sdas_compile_intent(const sdas_pipeline* p, const sdas_intent* in, sdas_candidate* out,
+                                uint32_t* objective_out) {
+  if (!p || !in || !out || !objective_out) return fail(SDAS_E_INVALID_ARG, "NULL argument");
+  if (in->objective > SDAS_INTENT_MIN_P90_LATENCY) return fail(SDAS_E_INVALID_ARG, "objective: bad enum");
+  if (in->objective == SDAS_INTENT_NONE && !in->rules)
+    return fail(SDAS_E_INVALID_ARG, "InvalidIntent: neither an objective nor explicit rules (SPEC.md:483)");
+  if (in->n_constraints && !in->constraints) return fail(SDAS_E_INVALID_ARG, "constraints: NULL");
+  const uint32_t nl = (uint32_t)p->links.size();
+  const uint32_t all_links = nl ? (1u << nl) - 1u : 0u;
+  sdas_candidate c;
+  if (in->rules) {
+    c = *in->rules;                                            // explicit rules pass through unchanged
+  } else {
+    memset(&c, 0, sizeof(c));
+    c.kind = SDAS_STATIC;
+    for (int l = 0; l < 8; ++l) c.mode[l] = 255;
+    c.metric = SDAS_METRIC_BUSY;
+    c.lo_permille = 400; c.hi_permille = 800; c.dwell_windows = 1;
+    c.band_mode[0] = SDAS_TOKEN; c.band_mode[1] = SDAS_FUNCTION; c.band_mode[2] = SDAS_BATCH;
+    c.band_mode[3] = SDAS_BATCH;
+    c.route_override = SDAS_ROUTE_NONE; c.q_hi = 2; c.select_role = -1; c.kv_policy = SDAS_KV_OFF;
+    c.guard_pct = 90;
+  }
+  uint32_t obj = SDAS_MIN_P99_E2E;
+  const uint64_t W = p->window ? p->window : 1;
+  if (in->objective == SDAS_INTENT_MAX_THROUGHPUT) {           // SPEC.md:478-479 three-band template
+    c.kind = SDAS_ADAPTIVE;
+    for (int l = 0; l < 8; ++l) c.mode[l] = 255;
+    c.ctl_links = all_links;
+    c.metric = SDAS_METRIC_BUSY;
+    c.lo_permille = 400; c.hi_permille = 800;
+    c.band_mode[0] = SDAS_TOKEN; c.band_mode[1] = SDAS_FUNCTION; c.band_mode[2] = SDAS_BATCH;
+    c.dwell_windows = (uint32_t)std::max<uint64_t>(1, (1000000ull + W - 1) / W);   // 1000 ms dwell
+    obj = SDAS_MAX_THROUGHPUT;
+  } else if (in->objective == SDAS_INTENT_MIN_P90_LATENCY) {   // SPEC.md:480 token_stream everywhere
+    c.kind = SDAS_STATIC;
+    for (uint32_t l = 0; l < 8; ++l) c.mode[l] = l < nl ? (uint8_t)SDAS_TOKEN : 255;
+    c.ctl_links = 0;
+    c.dwell_windows = (uint32_t)std::max<uint64_t>(1, (1000000ull + W - 1) / W);
+    obj = SDAS_MIN_P90_E2E;
+  }
+  for (uint32_t k = 0; k < in->n_constraints; ++k) {           // SPEC.md:480-481 constraint guards (M25)
+    const sdas_constraint& q = in->constraints[k];
+    if (q.metric > SDAS_CONSTRAINT_E2E_P99) return fail(SDAS_E_INVALID_ARG, "constraints[%u].metric: bad enum", k);
+    if (q.scope_links & ~all_links) return fail(SDAS_E_INVALID_ARG, "constraints[%u].scope_links: no such link", k);
+    const uint32_t pct = q.metric == SDAS_CONSTRAINT_E2E_P90 ? 90u : 99u;
+    const bool first = k == 0;
+    if (first && in->rules && (in->rules->batch_roles || in->rules->select_role >= 0) &&
+        in->rules->policy_slo_ticks != q.bound_ticks)
+      return fail(SDAS_E_LIMIT, "constraints[0].bound_ticks conflicts with the rules' policy_slo_ticks");
+    if (!first && (pct != c.guard_pct || q.bound_ticks != c.policy_slo_ticks))
+      return fail(SDAS_E_LIMIT, "constraints[%u]: one (metric, bound) per compiled policy", k);
+    c.guard_pct = pct;
+    c.policy_slo_ticks = q.bound_ticks;
+    c.guard_links |= q.scope_links ? q.scope_links : all_links;
+    c.kind = SDAS_ADAPTIVE;
+  }
+  *out = c;
+  *objective_out = obj;
   return ok();
 }
 
@@ -625,7 +700,8 @@ sdas_status sdas_metrics(const sdas_pipeline* p, const sdas_grid* grid, const sd
     out->makespan = u64(4); out->sum_e2e = u64(6); out->sum_ff = u64(8); out->int_nsys = u64(10);
     out->p50_e2e = w[12]; out->p99_e2e = w[13]; out->p50_ff = w[14]; out->p99_ff = w[15];
     out->bin_p50_e2e = w[16] & 0xFFFF; out->bin_p99_e2e = w[16] >> 16;
-    out->bin_p50_ff = w[17] & 0xFFFF; out->bin_p99_ff = w[17] >> 16;
+    out->bin_p50_ff = host_bin(w[14]); out->bin_p99_ff = host_bin(w[15]);   // derivable: not stored
+    out->p90_e2e = w[17];
     out->arrivals = w[20]; out->deliveries = w[21]; out->recv_steps = w[22]; out->decode_steps = w[23];
     out->window_closes = w[24]; out->mode_switches = w[25]; out->good = w[26]; out->large_items = w[27];
     out->tokens = u64(28);
@@ -670,6 +746,8 @@ sdas_status sdas_metrics(const sdas_pipeline* p, const sdas_grid* grid, const sd
     };
     pct(h, 50, &out->p50_e2e, &out->bin_p50_e2e);
     pct(h, 99, &out->p99_e2e, &out->bin_p99_e2e);
+    uint32_t bin90;
+    pct(h, 90, &out->p90_e2e, &bin90);
     pct(h + SDAS_NBINS, 50, &out->p50_ff, &out->bin_p50_ff);
     pct(h + SDAS_NBINS, 99, &out->p99_ff, &out->bin_p99_ff);
     derive();

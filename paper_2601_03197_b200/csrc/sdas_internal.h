@@ -38,7 +38,7 @@ struct DCand {          // one candidate, 64 B
   uint8_t band[4];
   uint32_t route_override, batch_roles, q_hi;
   int32_t select_role;
-  uint32_t kv_policy;
+  uint8_t kv_policy, guard_links, guard_pct, pad0;   // guard: M25 (f3)
   uint64_t policy_slo;
 };
 

@@ -689,17 +689,32 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
 
     // ---------------------------------------------------------------- window close + control (M15, M16)
     auto control = [&](int32_t q) {
-      for (uint32_t l = 0; l < n_links; ++l) {  // (i) three-band mode policy
-        if (!((cd.ctl_links >> l) & 1u)) continue;
-        const DRole& Rd = P.role[P.link[l].dst];
-        const bool mine = lane >= (int)Rd.first && lane < (int)(Rd.first + Rd.n);
-        const unsigned long long u =
-            warp_sum64(mine ? (cd.metric_load ? acc_lint : (unsigned long long)acc_busy) : 0ull);
-        const unsigned long long lhs = u * 1000ull;
-        uint32_t band = 1;
-        if (lhs >= (unsigned long long)cd.hi * P.window * Rd.n) band = 2;
-        else if (lhs <= (unsigned long long)cd.lo * P.window * Rd.n) band = 0;
-        const uint32_t want = cd.band[band], curm = (modes >> (2 * l)) & 3u;
+      const uint32_t w_n = H->w_n;
+      // M25 (f3): the guarded quantile of this window's completions violates policy_slo
+      const bool gviol = cd.guard_links && w_n >= 1 &&
+                         H->w_good < (uint32_t)(((unsigned long long)cd.guard_pct * w_n + 99ull) / 100ull);
+      for (uint32_t l = 0; l < n_links; ++l) {  // (i) three-band mode policy / (M25) guard, one decision
+        const bool ctl = (cd.ctl_links >> l) & 1u, grd = (cd.guard_links >> l) & 1u;
+        if (!ctl && !grd) continue;
+        uint32_t want;
+        if (grd && gviol) {
+          want = SDAS_BATCH;
+        } else if (ctl) {
+          const DRole& Rd = P.role[P.link[l].dst];
+          const bool mine = lane >= (int)Rd.first && lane < (int)(Rd.first + Rd.n);
+          const unsigned long long u =
+              warp_sum64(mine ? (cd.metric_load ? acc_lint : (unsigned long long)acc_busy) : 0ull);
+          const unsigned long long lhs = u * 1000ull;
+          uint32_t band = 1;
+          if (lhs >= (unsigned long long)cd.hi * P.window * Rd.n) band = 2;
+          else if (lhs <= (unsigned long long)cd.lo * P.window * Rd.n) band = 0;
+          want = cd.band[band];
+        } else if (w_n >= 1) {
+          want = cd.mode[l] == 255 ? P.link[l].mode : cd.mode[l];   // reset to the initial mode
+        } else {
+          continue;
+        }
+        const uint32_t curm = (modes >> (2 * l)) & 3u;
         const int32_t ql = __shfl_sync(FULL, qlm, l);
         if (want != curm && q - ql >= (int32_t)cd.dwell) {
           modes = (modes & ~(3u << (2 * l))) | (want << (2 * l));
@@ -709,7 +724,6 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
         }
       }
       bool viol = false, calm = false;
-      const uint32_t w_n = H->w_n;
       if (w_n >= 1) {
         const uint32_t k99 = (uint32_t)((99ull * w_n + 99ull) / 100ull);
         viol = H->w_good < k99;
@@ -989,13 +1003,14 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
       }
       val = lo + prefix;
     };
-    uint32_t v50e = 0xFFFFFFFFu, v99e = 0xFFFFFFFFu, v50f = 0xFFFFFFFFu, v99f = 0xFFFFFFFFu;
-    uint32_t b50e = 0xFFFFu, b99e = 0xFFFFu, b50f = 0xFFFFu, b99f = 0xFFFFu;
+    uint32_t v50e = 0xFFFFFFFFu, v99e = 0xFFFFFFFFu, v50f = 0xFFFFFFFFu, v99f = 0xFFFFFFFFu, v90e = 0xFFFFFFFFu;
+    uint32_t b50e = 0xFFFFu, b99e = 0xFFFFu, b50f = 0xFFFFu, b99f = 0xFFFFu, b90e = 0xFFFFu;
     if (completed > 0) {
       const uint32_t k50 = (uint32_t)((50ull * completed + 99ull) / 100ull);
       const uint32_t k99 = (uint32_t)((99ull * completed + 99ull) / 100ull);
       select(he, 0, k50, v50e, b50e);
       select(he, 0, k99, v99e, b99e);
+      select(he, 0, (uint32_t)((90ull * completed + 99ull) / 100ull), v90e, b90e);
       select(hf, 1, k50, v50f, b50f);
       select(hf, 1, k99, v99f, b99f);
     }
@@ -1019,7 +1034,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
       stg[8] = (uint32_t)sum_ff; stg[9] = (uint32_t)(sum_ff >> 32);
       stg[10] = (uint32_t)int_nsys; stg[11] = (uint32_t)(int_nsys >> 32);
       stg[12] = v50e; stg[13] = v99e; stg[14] = v50f; stg[15] = v99f;
-      stg[16] = b50e | (b99e << 16); stg[17] = b50f | (b99f << 16);
+      stg[16] = b50e | (b99e << 16); stg[17] = v90e;
       stg[18] = h.max_e2e; stg[19] = n_sat;
       stg[20] = arrivals; stg[21] = deliv; stg[22] = recvs; stg[23] = decs;
       stg[24] = window_closes; stg[25] = mode_switches; stg[26] = good; stg[27] = larges;

@@ -217,7 +217,7 @@ __global__ void k3_group_argmin(const uint8_t* __restrict__ blob, const uint8_t*
     k.makespan = s[4] | ((unsigned long long)s[5] << 32);
     const bool ff = obj == SDAS_MIN_P99_FF;
     k.sum = ff ? (s[8] | ((unsigned long long)s[9] << 32)) : (s[6] | ((unsigned long long)s[7] << 32));
-    k.p = obj == SDAS_MIN_P50_E2E ? s[12] : (ff ? s[15] : s[13]);
+    k.p = obj == SDAS_MIN_P50_E2E ? s[12] : obj == SDAS_MIN_P90_E2E ? s[17] : (ff ? s[15] : s[13]);
     k.good = s[26];
     k.large = s[27];
     if (!have || better(k, bk, obj, slo)) { bk = k; have = true; }
@@ -239,7 +239,7 @@ __global__ void k4_cell_pct(const uint8_t* __restrict__ blob, const int* __restr
   const unsigned long long n = warp_sum64(part);
   uint32_t p = 0xFFFFFFFFu;
   if (n > 0) {
-    const unsigned long long num = obj == SDAS_MIN_P50_E2E ? 50ull : 99ull;
+    const unsigned long long num = obj == SDAS_MIN_P50_E2E ? 50ull : obj == SDAS_MIN_P90_E2E ? 90ull : 99ull;
     const unsigned long long kq = (num * n + 99ull) / 100ull;
     unsigned long long incl = part;
 #pragma unroll

@@ -30,7 +30,10 @@ def _kv_fields(pipe):
 
 
 ARRIVALS = {"poisson": 0, "mmpp2": 1, "det": 2, "list": 3}
-OBJECTIVES = {"p99_e2e": 0, "p50_e2e": 1, "p99_ff": 2, "throughput": 3, "goodput": 4, "large_under_slo": 5}
+OBJECTIVES = {"p99_e2e": 0, "p50_e2e": 1, "p99_ff": 2, "throughput": 3, "goodput": 4, "large_under_slo": 5,
+              "p90_e2e": 6}
+INTENTS = {None: 0, "max_throughput": 1, "min_p90_latency": 2}
+CONSTRAINT_METRICS = {"e2e_p90": 0, "e2e_p99": 1}
 SCOPES = {"replica": 0, "cell": 1, "group": 2, "row": 3}
 FLAG_RECORDS, FLAG_SERIES, FLAG_TRACE, FLAG_STEPWISE = 1, 2, 4, 8
 NBINS, NCNT = 464, 24
@@ -40,8 +43,7 @@ SUMMARY_DTYPE = np.dtype([
     ("status", "<u4"), ("admitted", "<u4"), ("dropped", "<u4"), ("completed", "<u4"),
     ("makespan", "<u8"), ("sum_e2e", "<u8"), ("sum_ff", "<u8"), ("int_nsys", "<u8"),
     ("p50_e2e", "<u4"), ("p99_e2e", "<u4"), ("p50_ff", "<u4"), ("p99_ff", "<u4"),
-    ("bin_p50_e2e", "<u2"), ("bin_p99_e2e", "<u2"), ("bin_p50_ff", "<u2"), ("bin_p99_ff", "<u2"),
-    ("max_e2e", "<u4"), ("n_saturated", "<u4"),
+    ("bin_p50_e2e", "<u2"), ("bin_p99_e2e", "<u2"), ("p90_e2e", "<u4"), ("max_e2e", "<u4"), ("n_saturated", "<u4"),
     ("arrivals", "<u4"), ("deliveries", "<u4"), ("recv_steps", "<u4"), ("decode_steps", "<u4"),
     ("window_closes", "<u4"), ("mode_switches", "<u4"), ("good", "<u4"), ("large_items", "<u4"),
     ("tokens", "<u8"), ("batch_changes", "<u2"), ("select_changes", "<u2"), ("kv_transfers", "<u4")])
@@ -89,7 +91,16 @@ class Candidate(C.Structure):
                 ("lo_permille", C.c_uint32), ("hi_permille", C.c_uint32), ("dwell_windows", C.c_uint32),
                 ("band_mode", C.c_uint8 * 4), ("route_override", C.c_uint32), ("batch_roles", C.c_uint32),
                 ("q_hi", C.c_uint32), ("select_role", C.c_int32), ("kv_policy", C.c_uint32),
-                ("policy_slo_ticks", C.c_uint64)]
+                ("guard_links", C.c_uint32), ("guard_pct", C.c_uint32), ("policy_slo_ticks", C.c_uint64)]
+
+
+class Constraint(C.Structure):
+    _fields_ = [("metric", C.c_uint32), ("scope_links", C.c_uint32), ("bound_ticks", C.c_uint64)]
+
+
+class Intent(C.Structure):
+    _fields_ = [("objective", C.c_uint32), ("n_constraints", C.c_uint32),
+                ("constraints", C.POINTER(Constraint)), ("rules", C.POINTER(Candidate))]
 
 
 class ArrivalDesc(C.Structure):
@@ -130,7 +141,7 @@ class MetricsOut(C.Structure):
                 ("dropped", C.c_uint64), ("completed", C.c_uint64), ("p50_e2e", C.c_uint32),
                 ("p99_e2e", C.c_uint32), ("p50_ff", C.c_uint32), ("p99_ff", C.c_uint32),
                 ("bin_p50_e2e", C.c_uint32), ("bin_p99_e2e", C.c_uint32), ("bin_p50_ff", C.c_uint32),
-                ("bin_p99_ff", C.c_uint32), ("mean_e2e", C.c_double), ("mean_ff", C.c_double),
+                ("bin_p99_ff", C.c_uint32), ("p90_e2e", C.c_uint32), ("pad0", C.c_uint32), ("mean_e2e", C.c_double), ("mean_ff", C.c_double),
                 ("throughput", C.c_double), ("goodput", C.c_double)] + [
         (n, C.c_uint64) for n in ("makespan", "sum_e2e", "sum_ff", "int_nsys", "good", "large_items", "arrivals",
                                   "deliveries", "recv_steps", "decode_steps", "window_closes", "mode_switches",
@@ -140,7 +151,7 @@ class MetricsOut(C.Structure):
 
 EXPORTS = ["sdas_last_error", "sdas_version", "sdas_pipeline_create", "sdas_pipeline_destroy", "sdas_set",
            "sdas_reset", "sdas_get", "sdas_results_layout", "sdas_simulate", "sdas_control_sweep",
-           "sdas_group_argmin", "sdas_finalize", "sdas_metrics"]
+           "sdas_group_argmin", "sdas_finalize", "sdas_metrics", "sdas_compile_intent"]
 
 
 def lib():
@@ -171,6 +182,8 @@ def lib():
                                         C.c_void_p]
         L.sdas_metrics.argtypes = [C.c_void_p, C.POINTER(Grid), C.POINTER(Buffers), C.c_uint32, C.c_uint64,
                                    C.POINTER(MetricsOut)]
+        L.sdas_compile_intent.argtypes = [C.c_void_p, C.POINTER(Intent), C.POINTER(Candidate),
+                                          C.POINTER(C.c_uint32)]
         for f in EXPORTS:
             if f not in ("sdas_last_error", "sdas_version", "sdas_pipeline_destroy"):
                 getattr(L, f).restype = C.c_int32
@@ -208,7 +221,46 @@ def _candidate(c, n_links):
     x.select_role = -1 if c["select_role"] is None else c["select_role"]
     x.policy_slo_ticks = c["policy_slo"]
     x.kv_policy = KV_POLICIES[c.get("kv", "off")]
+    x.guard_links = sum(1 << l for l in c.get("guard_links", ()))
+    x.guard_pct = c.get("guard_pct", 90)
     return x
+
+
+def _candidate_dict(x, n_links):
+    """Inverse of _candidate: a ctypes sdas_candidate as a workloads candidate dict."""
+    inv = {v: k for k, v in MODES.items()}
+    kvinv = {v: k for k, v in KV_POLICIES.items()}
+    rinv = {v: k for k, v in ROUTES.items()}
+    return {"kind": "adaptive" if x.kind == 1 else "static",
+            "modes": [None if x.mode[l] == 255 else inv[x.mode[l]] for l in range(n_links)],
+            "ctl_links": [l for l in range(n_links) if (x.ctl_links >> l) & 1],
+            "metric": "load" if x.metric == 1 else "busy", "lo": x.lo_permille, "hi": x.hi_permille,
+            "dwell": x.dwell_windows, "band": [inv[x.band_mode[b]] for b in range(3)],
+            "route": None if x.route_override == ROUTE_NONE else rinv[x.route_override],
+            "batch_roles": [r for r in range(32) if (x.batch_roles >> r) & 1], "q_hi": x.q_hi,
+            "select_role": None if x.select_role < 0 else x.select_role, "policy_slo": x.policy_slo_ticks,
+            "kv": kvinv[x.kv_policy], "guard_links": [l for l in range(n_links) if (x.guard_links >> l) & 1],
+            "guard_pct": x.guard_pct}
+
+
+def compile_intent(pipeline, objective=None, constraints=(), rules=None):
+    """sdas_compile_intent (f3): an intent -> (candidate dict, sweep objective name).
+
+    objective: None | "max_throughput" | "min_p90_latency"; constraints: [(metric, bound_ticks, scope_links)]
+    with metric "e2e_p90" | "e2e_p99" and scope_links a list of link ids ([] = every link); rules: an
+    explicit candidate dict (passed through)."""
+    nl = len(pipeline.desc["links"])
+    cs = (Constraint * max(1, len(constraints)))()
+    for k, (m, bound, scope) in enumerate(constraints):
+        cs[k] = Constraint(CONSTRAINT_METRICS[m], sum(1 << l for l in scope), bound)
+    it = Intent(INTENTS[objective], len(constraints), C.cast(cs, C.POINTER(Constraint)), None)
+    keep = None
+    if rules is not None:
+        keep = _candidate(rules, nl)
+        it.rules = C.pointer(keep)
+    out, obj = Candidate(), C.c_uint32()
+    _check(lib().sdas_compile_intent(pipeline.h, C.byref(it), C.byref(out), C.byref(obj)))
+    return _candidate_dict(out, nl), {v: k for k, v in OBJECTIVES.items()}[obj.value]
 
 
 class GridView:

@@ -200,3 +200,35 @@ def test_coalesced_runs_equal_stepwise(cfg):
     assert np.array_equal(a["cells"][0], b["cells"][0]) and np.array_equal(a["cells"][1], b["cells"][1])
     if series:
         assert a["series"].tobytes() == b["series"].tobytes()
+
+
+# ------------------------------------------------------------------ f3: compiled intents, guard M25, p90
+def test_guard_alternation_toy():
+    p = W.toy_ht("token")
+    p["window"] = 1000
+    p["roles"][1]["cost"]["h"] = 40
+    cands = []
+    for bound, dwell in ((131, 1), (131, 2), (0, 1), (215, 1)):
+        c = W.static("token")
+        c.update(kind="adaptive", dwell=dwell, policy_slo=bound, guard_links=[0], guard_pct=90)
+        cands.append(c)
+    g = W.grid(cands, [W.arr_list([j * 1000 for j in range(7)], prompt=(4, 4), output=(4, 4))], n_requests=7,
+               series_stride=1, series_slots=4, series_windows=7)
+    gg, o = full_check(p, g, series=True)
+    assert [int(v) for v in gg["summary"]["mode_switches"]] == [6, 3, 1, 0]
+
+
+@pytest.mark.parametrize("objective", ["p90_e2e", "throughput"])
+def test_compiled_intent_grid(objective):
+    from paper_2601_03197_b200 import sdas
+    p = W.p2_x()
+    P = sdas.Pipeline(p)
+    cands = []
+    for obj in ("max_throughput", "min_p90_latency"):
+        for k in ([], [("e2e_p90", 3_000_000, [])], [("e2e_p99", 6_000_000, [])]):
+            cands.append(sdas.compile_intent(P, obj, constraints=k)[0])
+    cands.append(sdas.compile_intent(P, rules=W.static("batch"), constraints=[("e2e_p90", 2_500_000, [])])[0])
+    g = W.grid(cands, [W.poisson(m) for m in (1597600, 726182, 469882)], n_seeds=3, n_requests=300)
+    gg, o = full_check(p, g, objective=objective)
+    s = gg["summary"]
+    assert s["mode_switches"].sum() > 0 and (s["p90_e2e"][s["status"] == 0] > 0).all()
