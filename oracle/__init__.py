@@ -36,7 +36,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "liboracle.so")
 
 NBINS = 464
-NCNT = 24
+NCNT = 28
+NHIST = 3
 MAX_LINKS = 8
 
 MODES = {"batch": 0, "function": 1, "token": 2}
@@ -49,7 +50,7 @@ def _kv(pipe):
 ROUTES = {"jsq": 0, "rr": 1, "fixed": 2, "select": 3}
 ARRIVALS = {"poisson": 0, "mmpp2": 1, "det": 2, "list": 3}
 OBJECTIVES = {"p99_e2e": 0, "p50_e2e": 1, "p99_ff": 2, "throughput": 3, "goodput": 4, "large_under_slo": 5,
-              "p90_e2e": 6}
+              "p90_e2e": 6, "p99_e2e_int": 7}
 STATUS = {0: "ok", 1: "overflow", 2: "truncated"}
 CELL_FIELDS = ["n_replicas", "n_ok", "n_overflow", "n_truncated", "admitted", "dropped", "completed",
                "sum_e2e", "sum_ff", "makespan_sum", "int_nsys", "good", "large_items", "arrivals",
@@ -84,7 +85,8 @@ class Link(C.Structure):
 class Arrival(C.Structure):
     _fields_ = [("kind", C.c_uint32), ("gap", C.c_uint64 * 2), ("sojourn", C.c_uint64 * 2),
                 ("list", C.POINTER(C.c_uint64)), ("list_len", C.c_uint32), ("p_lo", C.c_uint32),
-                ("p_hi", C.c_uint32), ("o_lo", C.c_uint32), ("o_hi", C.c_uint32)]
+                ("p_hi", C.c_uint32), ("o_lo", C.c_uint32), ("o_hi", C.c_uint32),
+                ("interactive_permille", C.c_uint32)]
 
 
 class Candidate(C.Structure):
@@ -92,7 +94,8 @@ class Candidate(C.Structure):
                 ("metric_load", C.c_uint32), ("lo", C.c_uint32), ("hi", C.c_uint32), ("dwell", C.c_uint32),
                 ("band", C.c_uint32 * 3), ("route_override", C.c_uint32), ("batch_roles", C.c_uint32),
                 ("q_hi", C.c_uint32), ("select_role", C.c_int32), ("policy_slo", C.c_uint64),
-                ("kv_policy", C.c_uint32), ("guard_links", C.c_uint32), ("guard_pct", C.c_uint32)]
+                ("kv_policy", C.c_uint32), ("guard_links", C.c_uint32), ("guard_pct", C.c_uint32),
+                ("prio", C.c_uint32), ("admit", C.c_uint32), ("admit_lo", C.c_uint32), ("admit_hi", C.c_uint32)]
 
 
 class Pipeline(C.Structure):
@@ -120,6 +123,8 @@ SUMMARY_FIELDS = [
     ("window_closes", np.uint32), ("mode_switches", np.uint32), ("good", np.uint32), ("large_items", np.uint32),
     ("tokens", np.uint64), ("stop_tick", np.uint64), ("replica", np.uint64),
     ("batch_changes", np.uint32), ("select_changes", np.uint32), ("kv_transfers", np.uint32), ("p90_e2e", np.uint32),
+    ("completed_int", np.uint32), ("rejected", np.uint32), ("good_int", np.uint32), ("gate_changes", np.uint32),
+    ("sum_e2e_int", np.uint64), ("p50_e2e_int", np.uint32), ("p99_e2e_int", np.uint32),
     ("msgs_emitted", np.uint64), ("tokens_emitted", np.uint64), ("msgs_received", np.uint64),
     ("tokens_received", np.uint64),
 ]
@@ -184,6 +189,7 @@ def _arrival(a, keep):
         x.list_len = len(a["list"])
     x.p_lo, x.p_hi = a["prompt"]
     x.o_lo, x.o_hi = a["output"]
+    x.interactive_permille = a.get("interactive", 0)
     return x
 
 
@@ -207,6 +213,9 @@ def _candidate(c, n_links):
     x.kv_policy = KV_POLICIES[c.get("kv", "off")]
     x.guard_links = sum(1 << l for l in c.get("guard_links", ()))
     x.guard_pct = c.get("guard_pct", 90)
+    x.prio = 1 if c.get("prio") else 0
+    x.admit = 1 if c.get("admit") else 0
+    x.admit_lo, x.admit_hi = c.get("admit_band", (400, 800))
     return x
 
 
@@ -264,7 +273,7 @@ def simulate(pipe, grid, ids=None, threads=None, records=True, hists=True, serie
     threads = threads or os.cpu_count() or 1
     summ = np.zeros(n, dtype=SUMMARY_DTYPE)
     rec = np.zeros((n, p.N, 2), dtype=np.uint32) if records else None
-    hst = np.zeros((n, 2, NBINS), dtype=np.uint32) if hists else None
+    hst = np.zeros((n, NHIST, NBINS), dtype=np.uint32) if hists else None
     ser = None
     if series and grid["series_stride"]:
         ser = np.zeros((grid["series_slots"], grid["series_windows"], p.n_inst), dtype=SERIES_DTYPE)
@@ -290,7 +299,7 @@ def cells(pipe, grid, res):
     assert len(res["ids"]) == p.R and res["hists"] is not None
     n_cells = p.I * p.K * p.C
     cnt = np.zeros((n_cells, NCNT), dtype=np.int64)
-    hist = np.zeros((n_cells, 2, NBINS), dtype=np.int64)
+    hist = np.zeros((n_cells, NHIST, NBINS), dtype=np.int64)
     lib().orc_cells(C.byref(p.grid), res["summary"].ctypes.data, res["hists"].ctypes.data, cnt.ctypes.data,
                     hist.ctypes.data)
     return cnt, hist

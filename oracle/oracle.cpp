@@ -256,7 +256,7 @@ struct Replica {
   uint32_t s_coord;
   orc_summary& S;
   uint32_t* rec;        // [N][2] or null
-  uint32_t* hist;       // [2][NBINS] (always provided internally)
+  uint32_t* hist;       // [3][NBINS]: e2e, ff, interactive e2e (always provided internally)
   orc_series* series;   // this replica's [windows][n_inst] or null
   orc_trace* trace; uint64_t trace_cap; uint64_t* trace_n;
 
@@ -276,6 +276,10 @@ struct Replica {
   std::vector<uint32_t> o, nitems;
   std::vector<uint64_t> ff;
   std::vector<uint32_t> home;      // M21: KV home instance (index within the KV role) of request j
+  std::vector<uint8_t> cls;        // M26: 1 = interactive, 0 = background
+  std::vector<uint32_t> ve_int;    // M29: interactive e2e values (saturated u32)
+  bool gate_closed = false;        // M28: admission is interactive-only
+  int64_t q_last_gate = INT64_MIN / 2;
 
   std::priority_queue<Event, std::vector<Event>, std::greater<Event>> heap;
   uint64_t seq = 0, t = 0;
@@ -354,6 +358,13 @@ struct Replica {
     if (rec) { rec[2 * S.completed] = e32; rec[2 * S.completed + 1] = f32; }
     hist[bin_of(e32)]++;
     hist[ORC_NBINS + bin_of(f32)]++;
+    if (cls[j]) {                    // M29 per-class metrics
+      hist[2 * ORC_NBINS + bin_of(e32)]++;
+      S.completed_int++;
+      S.sum_e2e_int += e2e;
+      if (e2e <= P.slo) S.good_int++;
+      ve_int.push_back(e32);
+    }
     S.completed++;
     S.sum_e2e += e2e;
     S.sum_ff += f32;
@@ -447,8 +458,13 @@ struct Replica {
     Inst& I = inst[i];
     const orc_role& R = P.roles[I.role];
     if (!I.inbox.empty()) {  // RECV-first
-      Msg m = I.inbox.front();
-      I.inbox.pop_front();
+      // M27: with priority service, the first interactive message, else the head (FIFO per class)
+      size_t at = 0;
+      if (cand.prio)
+        for (size_t k = 0; k < I.inbox.size(); ++k)
+          if (cls[I.inbox[k].j]) { at = k; break; }
+      Msg m = I.inbox[at];
+      I.inbox.erase(I.inbox.begin() + (long)at);
       uint64_t cost = (uint64_t)I.c.h + (uint64_t)I.c.beta * m.tokens;
       if (m.opens) {
         uint32_t ord = nitems[m.j]++;
@@ -477,10 +493,14 @@ struct Replica {
       return;
     }
     while (I.batch.size() < I.B && !I.wait.empty()) {  // FIFO admission; modes bound here (M9)
+      size_t at = 0;                                   // M27: interactive first with priority service
+      if (cand.prio)
+        for (size_t k = 0; k < I.wait.size(); ++k)
+          if (cls[I.wait[k].first]) { at = k; break; }
       Item it{};
-      it.j = I.wait.front().first;
-      it.out = I.wait.front().second;
-      I.wait.pop_front();
+      it.j = I.wait[at].first;
+      it.out = I.wait[at].second;
+      I.wait.erase(I.wait.begin() + (long)at);
       const std::vector<uint32_t>& ol = out_links[I.role];
       for (size_t q = 0; q < ol.size(); ++q) it.mode[q] = cur_mode[ol[q]];
       I.batch.push_back(it);
@@ -497,6 +517,12 @@ struct Replica {
 
   void arrive(uint32_t j) {  // phase ARRIVE (M14)
     S.arrivals++;
+    if (gate_closed && !cls[j]) {   // M28: interactive-only admission rejects a background request
+      S.dropped++;
+      S.rejected++;
+      tr(TR_ARRIVE, j, 2, 0xFFFFFFFFu);
+      return;
+    }
     if (nsys >= P.request_cap) {
       S.dropped++;
       tr(TR_ARRIVE, j, 0, 0xFFFFFFFFu);
@@ -609,6 +635,20 @@ struct Replica {
         }
       }
     }
+    // (iv) M28 admission gate on the source role's busy time, dwell and no-op as M16
+    if (cand.admit) {
+      uint64_t u = 0;
+      for (uint32_t x = 0; x < role_n[0]; ++x) u += inst[role_first[0] + x].w_busy;
+      bool want = gate_closed;
+      if ((u128)u * 1000u >= (u128)cand.admit_hi * W * role_n[0]) want = true;
+      else if ((u128)u * 1000u <= (u128)cand.admit_lo * W * role_n[0]) want = false;
+      if (want != gate_closed && q - q_last_gate >= (int64_t)cand.dwell) {
+        gate_closed = want;
+        q_last_gate = q;
+        S.gate_changes++;
+        tr(TR_CONTROL, 3, 0, want ? 1u : 0u);
+      }
+    }
     // (iii) model selection (SELECT routing target)
     if (cand.select_role >= 0) {
       uint32_t r = (uint32_t)cand.select_role;
@@ -685,6 +725,15 @@ struct Replica {
     if (gen_arrivals(arr, G.master_seed, s_coord, N, A, Pj, Oj) != 0) return -1;
     o.assign(N, 0); nitems.assign(N, 0); ff.assign(N, UINT64_MAX);
     home.assign(N, 0);
+    cls.assign(N, 0);
+    if (arr.interactive_permille) {  // M26: class from ATTR draw sub-counter 1, word 0
+      const uint64_t thr = ((uint64_t)arr.interactive_permille << 32) / 1000;
+      for (uint32_t j = 0; j < N; ++j) {
+        uint32_t w[4];
+        draw(G.master_seed, j, s_coord, K_ATTR, 0, 1, w);
+        cls[j] = (uint64_t)w[0] < thr ? 1 : 0;
+      }
+    }
     if (P.kv_role) {  // M21: KV home of every request, from ATTR words 2 and 3
       const uint64_t skew32 = ((uint64_t)P.kv_home_skew << 32) / 1000;
       for (uint32_t j = 0; j < N; ++j) {
@@ -745,8 +794,9 @@ struct Replica {
       S.status = ORC_OVERFLOW;
       S.stop_tick = tk;
       S.replica = r;
-      std::memset(hist, 0, sizeof(uint32_t) * 2 * ORC_NBINS);
+      std::memset(hist, 0, sizeof(uint32_t) * ORC_NHIST * ORC_NBINS);
       S.p50_e2e = S.p99_e2e = S.p50_ff = S.p99_ff = 0xFFFFFFFFu;
+      S.p50_e2e_int = S.p99_e2e_int = 0xFFFFFFFFu;
       S.bin_p50_e2e = S.bin_p99_e2e = S.bin_p50_ff = S.bin_p99_ff = 0xFFFFu;
       S.p90_e2e = 0xFFFFFFFFu;
       return 0;
@@ -778,6 +828,14 @@ struct Replica {
     pct(ve, hist, 90, S.p90_e2e, bin90);
     pct(vf, hist + ORC_NBINS, 50, S.p50_ff, S.bin_p50_ff);
     pct(vf, hist + ORC_NBINS, 99, S.p99_ff, S.bin_p99_ff);
+    // M29: exact nearest-rank percentiles over the interactive completions alone
+    S.p50_e2e_int = S.p99_e2e_int = 0xFFFFFFFFu;
+    if (!ve_int.empty()) {
+      std::sort(ve_int.begin(), ve_int.end());
+      uint64_t n = ve_int.size();
+      S.p50_e2e_int = ve_int[(50 * n + 99) / 100 - 1];
+      S.p99_e2e_int = ve_int[(99 * n + 99) / 100 - 1];
+    }
     return 0;
   }
 };
@@ -848,7 +906,7 @@ int orc_simulate(const orc_pipeline* p, const orc_grid* g, const uint64_t* ids, 
   std::atomic<uint64_t> next(0);
   std::atomic<int> err(0);
   auto worker = [&]() {
-    std::vector<uint32_t> hbuf(2 * ORC_NBINS);
+    std::vector<uint32_t> hbuf(ORC_NHIST * ORC_NBINS);
     std::vector<uint32_t> rbuf;
     for (;;) {
       uint64_t x = next.fetch_add(1);
@@ -858,8 +916,8 @@ int orc_simulate(const orc_pipeline* p, const orc_grid* g, const uint64_t* ids, 
       uint32_t s = (uint32_t)(g_idx % g->n_seeds) + g->seed_offset;
       const orc_candidate& c = g->cand[rid % g->n_cand];
       std::memset(&out[x], 0, sizeof(orc_summary));
-      uint32_t* h = hists ? hists + x * 2 * ORC_NBINS : hbuf.data();
-      std::memset(h, 0, sizeof(uint32_t) * 2 * ORC_NBINS);
+      uint32_t* h = hists ? hists + x * ORC_NHIST * ORC_NBINS : hbuf.data();
+      std::memset(h, 0, sizeof(uint32_t) * ORC_NHIST * ORC_NBINS);
       uint32_t* rec;
       if (records) rec = records + x * 2ull * g->n_requests;
       else { rbuf.assign(2ull * g->n_requests, 0); rec = rbuf.data(); }
@@ -887,7 +945,7 @@ void orc_cells(const orc_grid* g, const orc_summary* sums, const uint32_t* hists
   uint64_t C = g->n_cand, S = g->n_seeds, K = g->n_profiles, I = g->n_rates;
   uint64_t n_cells = I * K * C;
   std::memset(cnt, 0, sizeof(int64_t) * n_cells * ORC_NCNT);
-  std::memset(hist, 0, sizeof(int64_t) * n_cells * 2 * ORC_NBINS);
+  std::memset(hist, 0, sizeof(int64_t) * n_cells * ORC_NHIST * ORC_NBINS);
   for (uint64_t r = 0; r < I * K * S * C; ++r) {
     uint64_t c = r % C, gg = r / C, ik = gg / S;
     uint64_t cell = ik * C + c;
@@ -902,7 +960,9 @@ void orc_cells(const orc_grid* g, const orc_summary* sums, const uint32_t* hists
     q[14] += x.deliveries; q[15] += x.recv_steps; q[16] += x.decode_steps; q[17] += x.window_closes;
     q[18] += x.mode_switches; q[19] += x.tokens; q[20] += x.batch_changes; q[21] += x.select_changes;
     q[22] += x.n_saturated; q[23] += x.kv_transfers;
-    for (int b = 0; b < 2 * ORC_NBINS; ++b) hist[cell * 2 * ORC_NBINS + b] += hists[r * 2 * ORC_NBINS + b];
+    q[24] += x.completed_int; q[25] += x.rejected; q[26] += x.sum_e2e_int; q[27] += x.good_int;
+    for (int b = 0; b < ORC_NHIST * ORC_NBINS; ++b)
+      hist[cell * ORC_NHIST * ORC_NBINS + b] += hists[r * ORC_NHIST * ORC_NBINS + b];
   }
 }
 
@@ -939,6 +999,10 @@ bool better(const Key& a, const Key& b, uint32_t obj, uint64_t slo) {
       if (a.p != b.p) return a.p < b.p;
       break;
     }
+    case ORC_OBJ_P99_E2E_INT:   // interactive latency only: background drops are the gate's business
+      if (a.p != b.p) return a.p < b.p;
+      if (a.sum != b.sum) return a.sum < b.sum;
+      break;
     default:
       if (a.dropped != b.dropped) return a.dropped < b.dropped;
       if (a.p != b.p) return a.p < b.p;
@@ -963,8 +1027,8 @@ void orc_argmin_groups(const orc_grid* g, const orc_summary* sums, uint32_t obj,
       k.bad = x.status != ORC_OK;
       k.dropped = x.dropped;
       k.p = obj == ORC_OBJ_P50_E2E ? x.p50_e2e : obj == ORC_OBJ_P99_FF ? x.p99_ff
-          : obj == ORC_OBJ_P90_E2E ? x.p90_e2e : x.p99_e2e;
-      k.sum = obj == ORC_OBJ_P99_FF ? x.sum_ff : x.sum_e2e;
+          : obj == ORC_OBJ_P90_E2E ? x.p90_e2e : obj == ORC_OBJ_P99_E2E_INT ? x.p99_e2e_int : x.p99_e2e;
+      k.sum = obj == ORC_OBJ_P99_FF ? x.sum_ff : obj == ORC_OBJ_P99_E2E_INT ? x.sum_e2e_int : x.sum_e2e;
       k.completed = x.completed; k.makespan = x.makespan; k.good = x.good; k.large = x.large_items;
       k.c = (uint32_t)c;
       if (bc < 0 || better(k, bk, obj, slo)) { bk = k; bc = (int32_t)c; }
@@ -983,7 +1047,8 @@ void orc_argmin_rows(const orc_grid* g, const int64_t* cnt, const int64_t* hist,
     for (uint64_t c = 0; c < C; ++c) {
       uint64_t cell = row * C + c;
       const int64_t* q = cnt + cell * ORC_NCNT;
-      const int64_t* h = hist + cell * 2 * ORC_NBINS + (obj == ORC_OBJ_P99_FF ? ORC_NBINS : 0);
+      const int64_t* h = hist + cell * ORC_NHIST * ORC_NBINS +
+                         (obj == ORC_OBJ_P99_FF ? ORC_NBINS : obj == ORC_OBJ_P99_E2E_INT ? 2 * ORC_NBINS : 0);
       uint64_t n = 0;
       for (int b = 0; b < ORC_NBINS; ++b) n += (uint64_t)h[b];
       uint64_t p = 0xFFFFFFFFull;
@@ -999,7 +1064,7 @@ void orc_argmin_rows(const orc_grid* g, const int64_t* cnt, const int64_t* hist,
       k.bad = q[1] != q[0];
       k.dropped = (uint64_t)q[5];
       k.p = p;
-      k.sum = (uint64_t)(obj == ORC_OBJ_P99_FF ? q[8] : q[7]);
+      k.sum = (uint64_t)(obj == ORC_OBJ_P99_FF ? q[8] : obj == ORC_OBJ_P99_E2E_INT ? q[26] : q[7]);
       k.completed = (uint64_t)q[6]; k.makespan = (uint64_t)q[9]; k.good = (uint64_t)q[11];
       k.large = (uint64_t)q[12];
       k.c = (uint32_t)c;

@@ -23,7 +23,7 @@ enum { ORC_POISSON = 0, ORC_MMPP2 = 1, ORC_DET = 2, ORC_LIST = 3 };
 enum { ORC_OK = 0, ORC_OVERFLOW = 1, ORC_TRUNCATED = 2 };
 enum { ORC_KV_OFF = 0, ORC_KV_AFFINITY = 1, ORC_KV_RECOMPUTE = 2, ORC_KV_POSTHOC = 3, ORC_KV_HINT = 4 };
 enum { ORC_OBJ_P99_E2E = 0, ORC_OBJ_P50_E2E = 1, ORC_OBJ_P99_FF = 2, ORC_OBJ_THROUGHPUT = 3,
-       ORC_OBJ_GOODPUT = 4, ORC_OBJ_LARGE_UNDER_SLO = 5, ORC_OBJ_P90_E2E = 6 };
+       ORC_OBJ_GOODPUT = 4, ORC_OBJ_LARGE_UNDER_SLO = 5, ORC_OBJ_P90_E2E = 6, ORC_OBJ_P99_E2E_INT = 7 };
 
 #define ORC_NBINS 464
 #define ORC_MAX_LINKS 8
@@ -49,6 +49,7 @@ typedef struct {
   uint64_t gap[2], sojourn[2];
   const uint64_t* list; uint32_t list_len;
   uint32_t p_lo, p_hi, o_lo, o_hi;
+  uint32_t interactive_permille;  /* M26 (f2): share of interactive requests, 0..1000 */
 } orc_arrival;
 
 typedef struct {
@@ -66,6 +67,9 @@ typedef struct {
   uint32_t kv_policy;             /* ORC_KV_* (rules M21-M24) */
   uint32_t guard_links;           /* M25 (f3): links flipped to BATCH while the window e2e quantile */
   uint32_t guard_pct;             /*   guard_pct (e.g. 90) exceeds policy_slo; else reset to base  */
+  uint32_t prio;                  /* M27 (f2): serve interactive first at every inbox and wait queue */
+  uint32_t admit;                 /* M28 (f2): admission gate on the source role's busy fraction */
+  uint32_t admit_lo, admit_hi;    /*   reopen at <= lo, interactive-only at >= hi (permille) */
 } orc_candidate;
 
 typedef struct {
@@ -97,6 +101,9 @@ typedef struct {
   uint64_t stop_tick;
   uint64_t replica;
   uint32_t batch_changes, select_changes, kv_transfers, p90_e2e;   /* p90_e2e: exact nearest rank (f3) */
+  uint32_t completed_int, rejected, good_int, gate_changes;   /* M29 (f2) per-class metrics */
+  uint64_t sum_e2e_int;
+  uint32_t p50_e2e_int, p99_e2e_int;
   uint64_t msgs_emitted, tokens_emitted;     /* conservation checks */
   uint64_t msgs_received, tokens_received;
 } orc_summary;
@@ -126,7 +133,7 @@ uint32_t orc_mode_step(uint64_t u, uint32_t lo, uint32_t hi, uint64_t window, ui
 /* --- the simulation ---------------------------------------------------------------- */
 /* Runs replicas `ids[0..n)` (global ids r = g*C + c, g = (i*K + k)*S + s).
  * records: NULL or [n * n_requests] x {e2e u32, ff u32}
- * hists:   NULL or [n * 2 * ORC_NBINS] u32 (e2e then ff)
+ * hists:   NULL or [n * ORC_NHIST * ORC_NBINS] u32 (e2e, ff, interactive e2e)
  * series:  NULL or [series_slots * series_windows * n_inst] (indexed by r / stride)
  * trace:   NULL or [trace_cap] for replica trace_id; *trace_n receives the count
  * Returns 0 on success, <0 on invalid input. */
@@ -136,8 +143,9 @@ int orc_simulate(const orc_pipeline* p, const orc_grid* g, const uint64_t* ids, 
                  uint64_t* trace_n);
 
 /* Cell merge over a full grid (cells indexed (i*K + k)*C + c): cnt [n_cells * ORC_NCNT] i64,
- * hist [n_cells * 2 * ORC_NBINS] i64.  summaries/hists indexed by global replica id. */
-#define ORC_NCNT 24
+ * hist [n_cells * ORC_NHIST * ORC_NBINS] i64.  summaries/hists indexed by global replica id. */
+#define ORC_NCNT 28
+#define ORC_NHIST 3
 void orc_cells(const orc_grid* g, const orc_summary* sums, const uint32_t* hists, int64_t* cnt,
                int64_t* hist);
 /* Per-group argmin (M20): best[g] = winning candidate c; per-row argmin over pooled cells. */

@@ -333,3 +333,36 @@ def config_kv(n_seeds=8, n_requests=1000, gaps=(1000000, 500000, 350000, 280000,
     hinted transfer, over request rates."""
     cands = [with_kv(static("batch"), k) for k in KV_POLICIES]
     return p2_kv(), grid(cands, [poisson(m) for m in gaps], n_seeds=n_seeds, n_requests=n_requests)
+
+
+# ------------------------------------------------------------------ f2: priority classes and admission
+def with_classes(arrival, interactive_permille):
+    """An arrival profile whose requests are interactive with probability permille/1000 (M26)."""
+    a = copy.deepcopy(arrival)
+    a["interactive"] = int(interactive_permille)
+    return a
+
+
+def with_prio(cand, prio=True, admit=False, admit_band=(400, 800)):
+    """Candidate with M27 priority service and/or the M28 admission gate (the gate needs ADAPTIVE)."""
+    c = copy.deepcopy(cand)
+    c["prio"] = bool(prio)
+    c["admit"] = bool(admit)
+    c["admit_band"] = tuple(admit_band)
+    if admit:
+        c["kind"] = "adaptive"
+    return c
+
+
+def config_prio(n_seeds=8, n_requests=1000, interactive=300,
+                gaps=(1597600, 726182, 469882, 399400, 347304)):
+    """f2 workload: P2-X with an interactive share; FIFO vs interactive-first service x admission gate
+    (PAPER.md:49/126 pipeline-wide prioritization, "admit only high-priority requests under
+    load") x BATCH / TOKEN."""
+    cands = []
+    for mode in ("batch", "token"):
+        for prio in (False, True):
+            for admit in (False, True):
+                cands.append(with_prio(static(mode), prio, admit, (500, 850)))
+    arrs = [with_classes(poisson(g), interactive) for g in gaps]
+    return p2_x(), grid(cands, arrs, n_seeds=n_seeds, n_requests=n_requests)
