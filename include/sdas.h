@@ -57,7 +57,8 @@ enum { SDAS_METRIC_BUSY = 0, SDAS_METRIC_LOAD = 1 };
 enum { SDAS_REPLICA_OK = 0, SDAS_REPLICA_OVERFLOW = 1, SDAS_REPLICA_TRUNCATED = 2 };
 enum { SDAS_MIN_P99_E2E = 0, SDAS_MIN_P50_E2E = 1, SDAS_MIN_P99_FF = 2, SDAS_MAX_THROUGHPUT = 3,
        SDAS_MAX_GOODPUT = 4, SDAS_MAX_LARGE_FRAC_UNDER_SLO = 5,
-       SDAS_MIN_P90_E2E = 6 };                                               /* rule M20 (+ f3 p90) */
+       SDAS_MIN_P90_E2E = 6,                                                 /* f3: exact p90 */
+       SDAS_MIN_P99_E2E_INTERACTIVE = 7 };                                   /* f2: M29 */
 enum { SDAS_SCOPE_REPLICA = 0, SDAS_SCOPE_CELL = 1, SDAS_SCOPE_GROUP = 2, SDAS_SCOPE_ROW = 3 };
 
 #define SDAS_FLAG_RECORDS 1u /* write per-request (e2e, ff) records to buffers.records */
@@ -74,8 +75,9 @@ enum { SDAS_SCOPE_REPLICA = 0, SDAS_SCOPE_CELL = 1, SDAS_SCOPE_GROUP = 2, SDAS_S
 #define SDAS_MAX_BATCH 32    /* max_num_seqs upper bound: one lane per sequence */
 #define SDAS_MAX_REQUESTS 65535
 #define SDAS_NBINS 464       /* rule M17: log-linear bins over u32 latencies */
-#define SDAS_NCNT 24         /* int64 counters per cell */
-#define SDAS_SUMMARY_BYTES 128
+#define SDAS_NCNT 28         /* int64 counters per cell */
+#define SDAS_NHIST 3         /* histograms per cell: e2e, first feedback, interactive e2e (M29) */
+#define SDAS_SUMMARY_BYTES 160
 
 /* ---- pipeline description ---------- */
 typedef struct {           /* per-message and per-token service model of one agent instance */
@@ -160,6 +162,11 @@ typedef struct {
                                  ceil(guard_pct * n / 100) of a window's n >= 1 completions met
                                  policy_slo_ticks, else reset to their initial mode (needs ADAPTIVE) */
   uint32_t guard_pct;         /* 0..100: the guarded end-to-end quantile (90 = p90) */
+  uint32_t prio;              /* M27 (f2): 1 = every inbox and decode-wait queue serves interactive
+                                 requests first (FIFO within a class); 0 = FIFO over both classes */
+  uint32_t admit;             /* M28 (f2): 1 = admission gate (agent-level rule "admit only high-priority
+                                 requests under load"), needs ADAPTIVE */
+  uint32_t admit_lo_permille, admit_hi_permille; /* gate opens at <= lo, interactive-only at >= hi */
   uint64_t policy_slo_ticks;  /* SLO used by the controller's window p99 test */
 } sdas_candidate;
 
@@ -170,6 +177,7 @@ typedef struct {
   const uint64_t* list;       /* LIST: nondecreasing arrival ticks, list_len >= n_requests */
   uint32_t list_len;
   uint32_t prompt_lo, prompt_hi, out_lo, out_hi; /* P ~ U[lo,hi], O ~ U[lo,hi] (M5), <= 65535 */
+  uint32_t interactive_permille; /* M26 (f2): share of interactive requests, 0..1000 (0 = one class) */
 } sdas_arrival_desc;
 
 typedef struct {
@@ -191,19 +199,21 @@ typedef struct {
 typedef struct {
   uint64_t params_bytes;     /* device: packed descriptors (written by the library) */
   uint64_t work_bytes;       /* device: scratch (replica counter + per-warp record scratch) */
-  uint64_t summary_bytes;    /* device: n_local_replicas x 128-byte summary records, little-endian u32 words:
+  uint64_t summary_bytes;    /* device: n_local_replicas x 160-byte summary records, little-endian u32 words:
                                 0 status, 1 admitted, 2 dropped, 3 completed, 4-5 makespan (or overflow tick),
                                 6-7 sum e2e, 8-9 sum ff, 10-11 integral N_sys dt, 12-15 p50/p99 e2e, p50/p99 ff,
                                 16 bins of p50/p99 e2e (u16 pair), 17 exact p90 e2e (f3), 18 max e2e, 19 saturated records, 20 arrivals,
                                 21 deliveries, 22 RECV steps, 23 DECODE steps, 24 window closes, 25 mode
                                 switches, 26 good, 27 large-model items, 28-29 output tokens, 30 batch|select
-                                changes (u16 pair), 31 KV transfers (M24) */
+                                changes (u16 pair), 31 KV transfers (M24); f2 (M29): 32 interactive
+                                completions, 33 rejected by the admission gate, 34-35 sum interactive e2e,
+                                36-37 exact p50/p99 interactive e2e, 38 interactive good, 39 gate changes */
   uint64_t records_bytes;    /* device: n_local_replicas x n_requests x {u32 e2e, u32 ff} (FLAG_RECORDS) */
   uint64_t series_bytes;     /* device: series_slots x series_windows x n_instances x 16 B (FLAG_SERIES);
                                 zeroed by sdas_simulate: windows a replica never reaches (it ended or
                                 overflowed first) read as 0 */
   uint64_t cell_cnt_bytes;   /* device: n_cells x SDAS_NCNT int64 (zeroed by the caller; accumulated) */
-  uint64_t cell_hist_bytes;  /* device: n_cells x 2 x SDAS_NBINS int32 (zeroed by the caller) */
+  uint64_t cell_hist_bytes;  /* device: n_cells x SDAS_NHIST x SDAS_NBINS int32 (zeroed by the caller) */
   uint64_t best_group_bytes; /* device: n_local_groups int32 (control_sweep) */
   uint64_t best_row_bytes;   /* device: n_rows int32 (finalize) */
   uint64_t trace_bytes;      /* device: 8 + trace_cap x 24 B (FLAG_TRACE) */
@@ -251,6 +261,8 @@ typedef struct {
   uint64_t makespan, sum_e2e, sum_ff, int_nsys, good, large_items;
   uint64_t arrivals, deliveries, recv_steps, decode_steps, window_closes, mode_switches, tokens;
   uint64_t message_events, des_events;            /* arrivals + deliveries; + steps + window closes */
+  uint64_t completed_int, rejected, sum_e2e_int, good_int;   /* f2 (M29) */
+  uint32_t p50_e2e_int, p99_e2e_int;              /* exact (REPLICA) or bin lower edge (CELL) */
   int32_t best;                                   /* GROUP / ROW scope: winning candidate */
   const uint8_t* series;                          /* REPLICA scope with FLAG_SERIES: 16 B records */
   uint64_t series_len;                            /* windows x instances */

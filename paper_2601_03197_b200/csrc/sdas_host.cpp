@@ -199,11 +199,20 @@ sdas_status plan(const sdas_pipeline* p, const sdas_grid* g, Plan& pl) {
       return fail(SDAS_E_INVALID_FIELD, "cand[%u].route_override: NONE, JSQ or RR", c);
     if (cd.metric > SDAS_METRIC_LOAD || cd.lo_permille > 1000000 || cd.hi_permille > 1000000 || cd.dwell_windows > (1u << 30))
       return fail(SDAS_E_INVALID_FIELD, "cand[%u]: metric/lo/hi/dwell out of range", c);
+    if (cd.prio > 1 || cd.admit > 1) return fail(SDAS_E_INVALID_FIELD, "cand[%u].prio/admit: 0 or 1", c);
+    if (cd.admit && (cd.kind != SDAS_ADAPTIVE || cd.admit_lo_permille > cd.admit_hi_permille ||
+                     cd.admit_hi_permille > 65535))
+      return fail(SDAS_E_INVALID_FIELD, "cand[%u].admit: needs ADAPTIVE and admit_lo <= admit_hi <= 65535", c);
   }
   const uint64_t nIK = (uint64_t)g->n_rates * g->n_profiles;
   for (uint64_t a = 0; a < nIK; ++a) {
     const sdas_arrival_desc& A = g->arrivals[a];
     if (A.kind > SDAS_LIST) return fail(SDAS_E_INVALID_FIELD, "arrivals[%llu].kind: bad enum", (unsigned long long)a);
+    if (A.interactive_permille > 1000)
+      return fail(SDAS_E_INVALID_FIELD, "arrivals[%llu].interactive_permille: 0..1000", (unsigned long long)a);
+    if (A.interactive_permille && p->kv_role)
+      return fail(SDAS_E_LIMIT, "arrivals[%llu]: request classes with KV modelling are not supported",
+                  (unsigned long long)a);
     if (A.prompt_lo > A.prompt_hi || A.prompt_hi > 65535 || A.out_lo > A.out_hi || A.out_hi > 65535)
       return fail(SDAS_E_INVALID_FIELD, "arrivals[%llu]: prompt/out ranges must be lo <= hi <= 65535",
                   (unsigned long long)a);
@@ -284,6 +293,9 @@ sdas_status plan(const sdas_pipeline* p, const sdas_grid* g, Plan& pl) {
     h.role[L.dst_role].in_link = (int32_t)l;
   }
   h.kv_role = p->kv_role;
+  h.cls = 0;
+  for (uint64_t a = 0; a < (uint64_t)g->n_rates * g->n_profiles; ++a)
+    if (g->arrivals[a].interactive_permille) h.cls = 1;
   h.kv_ctx = p->kv_ctx;
   h.kv_tau = p->kv_tau;
   h.kv_skew32 = ((uint64_t)p->kv_skew << 32) / 1000;
@@ -310,19 +322,20 @@ sdas_status plan(const sdas_pipeline* p, const sdas_grid* g, Plan& pl) {
   h.off_reqNit = (uint32_t)o; o += 2ull * R;
   h.off_reqOut = (uint32_t)o; o += 2ull * R;
   h.off_reqHome = (uint32_t)o; o += R;                    // u8 KV home per request slot (M21)
+  h.off_reqCls = (uint32_t)o; o += h.cls ? R : 0;         // u8 class per request slot (M26)
   o = align_up(o, 16);
   h.off_bitmap = (uint32_t)o; o += 4ull * h.bitmap_words;
   for (uint32_t i = 0; i < h.n_inst; ++i) {
     DInst& I = h.inst[i];
     o = align_up(o, 16);
-    I.off_inbox = (uint32_t)o; o += 8ull * I.inbox_cap;
+    I.off_inbox = (uint32_t)o; o += 8ull * I.inbox_cap * (h.cls ? 2 : 1);   // class-1 ring follows (M27)
     if (h.kv_role && I.role == h.kv_role) o += 4ull * I.inbox_cap;  // hinted-transfer ready ticks (M23)
     o = align_up(o, 16);
     I.off_ftick = (uint32_t)o; o += 4ull * I.flight_cap;
     o = align_up(o, 16);
     I.off_fbody = (uint32_t)o; o += 8ull * I.flight_cap;
     o = align_up(o, 16);
-    I.off_wait = (uint32_t)o; o += 4ull * I.wait_cap;
+    I.off_wait = (uint32_t)o; o += 4ull * I.wait_cap * (h.cls ? 2 : 1);
     o = align_up(o, 16);
     I.off_batch = (uint32_t)o; o += 4ull * 32 * h.role[I.role].batch_words;
   }
@@ -345,7 +358,7 @@ sdas_status plan(const sdas_pipeline* p, const sdas_grid* g, Plan& pl) {
     const uint64_t sb = h.off_warps + (uint64_t)wpb * h.smem_per_warp;
     if (sb > smem_cap) break;
     int bps = 0, nsm = 0;
-    if (query_occupancy(wpb, (uint32_t)sb, h.max_out, &bps, &nsm) == 0 && bps > 0) {
+    if (query_occupancy(wpb, (uint32_t)sb, h.max_out, h.cls, &bps, &nsm) == 0 && bps > 0) {
       have_dev = true;
       n_sm = nsm;
     } else {
@@ -363,11 +376,12 @@ sdas_status plan(const sdas_pipeline* p, const sdas_grid* g, Plan& pl) {
   const uint64_t want_blocks = (h.n_local_replicas + best_w - 1) / best_w;
   pl.blocks = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)n_sm * best_b, want_blocks));
   pl.total_warps = (uint64_t)pl.blocks * best_w;
+  h.off_rec_cls = sizeof(Work) + pl.total_warps * (uint64_t)g->n_requests * 8ull;
 
   // --- blob: DParams | candidates | arrivals | LIST ticks
   uint64_t b = align_up(sizeof(DParams), 64);
-  h.off_cand = b; b += 64ull * g->n_candidates;
-  h.off_arr = b; b += 64ull * nIK;
+  h.off_cand = b; b += sizeof(DCand) * (uint64_t)g->n_candidates;
+  h.off_arr = b; b += sizeof(DArr) * nIK;
   for (uint64_t a = 0; a < nIK; ++a)
     if (g->arrivals[a].kind == SDAS_LIST) b += 8ull * g->n_requests;
   pl.blob_bytes = align_up(b, 256);
@@ -391,16 +405,21 @@ void pack_blob(const sdas_grid* g, const Plan& pl, std::vector<uint8_t>& blob) {
     d.kv_policy = (uint8_t)s.kv_policy;
     d.guard_links = (uint8_t)s.guard_links;
     d.guard_pct = (uint8_t)s.guard_pct;
+    d.prio = s.prio ? 1u : 0u;
+    d.admit = s.admit ? 1u : 0u;
+    d.admit_lo = (uint16_t)s.admit_lo_permille;
+    d.admit_hi = (uint16_t)s.admit_hi_permille;
   }
   const uint64_t nIK = (uint64_t)g->n_rates * g->n_profiles;
   DArr* da = reinterpret_cast<DArr*>(blob.data() + pl.hp.off_arr);
-  uint64_t lo = pl.hp.off_arr + 64ull * nIK;
+  uint64_t lo = pl.hp.off_arr + sizeof(DArr) * nIK;
   for (uint64_t a = 0; a < nIK; ++a) {
     const sdas_arrival_desc& s = g->arrivals[a];
     DArr& d = da[a];
     d.kind = s.kind; d.list_len = s.list_len;
     d.gap0 = s.mean_gap[0]; d.gap1 = s.mean_gap[1]; d.soj0 = s.mean_sojourn[0]; d.soj1 = s.mean_sojourn[1];
     d.p_lo = s.prompt_lo; d.p_hi = s.prompt_hi; d.o_lo = s.out_lo; d.o_hi = s.out_hi;
+    d.ithr = ((uint64_t)s.interactive_permille << 32) / 1000;
     if (s.kind == SDAS_LIST) {
       d.list_off = lo;
       memcpy(blob.data() + lo, s.list, 8ull * g->n_requests);
@@ -413,14 +432,14 @@ sdas_status fill_layout(const Plan& pl, const sdas_grid* g, sdas_layout* L) {
   memset(L, 0, sizeof(*L));
   const DParams& h = pl.hp;
   L->params_bytes = pl.blob_bytes;
-  const uint64_t scratch = pl.total_warps * (uint64_t)g->n_requests * 8ull;
+  const uint64_t scratch = pl.total_warps * (uint64_t)g->n_requests * 9ull;   // records + class bytes
   L->work_bytes = align_up(sizeof(Work) + std::max<uint64_t>(scratch, pl.n_cells * 4ull), 256);
   L->summary_bytes = align_up(std::max<uint64_t>(1, h.n_local_replicas) * SDAS_SUMMARY_BYTES, 256);
   L->records_bytes = (g->flags & SDAS_FLAG_RECORDS) ? align_up(h.n_local_replicas * g->n_requests * 8ull, 256) : 0;
   L->series_bytes = (g->flags & SDAS_FLAG_SERIES)
                         ? align_up((uint64_t)g->series_slots * g->series_windows * h.n_inst * 16ull, 256) : 0;
   L->cell_cnt_bytes = align_up(pl.n_cells * SDAS_NCNT * 8ull, 256);
-  L->cell_hist_bytes = align_up(pl.n_cells * 2ull * SDAS_NBINS * 4ull, 256);
+  L->cell_hist_bytes = align_up(pl.n_cells * (uint64_t)SDAS_NHIST * SDAS_NBINS * 4ull, 256);
   L->best_group_bytes = align_up(std::max<uint64_t>(1, h.n_local_groups) * 4ull, 256);
   L->best_row_bytes = align_up(std::max<uint64_t>(1, pl.n_rows) * 4ull, 256);
   L->trace_bytes = (g->flags & SDAS_FLAG_TRACE) ? align_up(8ull + 24ull * g->trace_cap, 256) : 0;
@@ -563,7 +582,7 @@ sdas_status sdas_simulate(const sdas_pipeline* p, const sdas_grid* grid, const s
 
 sdas_status sdas_control_sweep(const sdas_pipeline* p, const sdas_grid* grid, uint32_t objective,
                                uint64_t objective_slo, const sdas_buffers* dev, void* stream) {
-  if (objective > SDAS_MIN_P90_E2E) return fail(SDAS_E_INVALID_ARG, "objective: bad enum");
+  if (objective > SDAS_MIN_P99_E2E_INTERACTIVE) return fail(SDAS_E_INVALID_ARG, "objective: bad enum");
   if (dev && !dev->best_group) return fail(SDAS_E_BUFFER, "control_sweep needs best_group");
   Plan pl;
   sdas_status s = run_sim(p, grid, dev, stream, pl);
@@ -576,7 +595,7 @@ sdas_status sdas_control_sweep(const sdas_pipeline* p, const sdas_grid* grid, ui
 
 sdas_status sdas_group_argmin(const sdas_pipeline* p, const sdas_grid* grid, uint32_t objective,
                               uint64_t objective_slo, const sdas_buffers* dev, void* stream) {
-  if (objective > SDAS_MIN_P90_E2E) return fail(SDAS_E_INVALID_ARG, "objective: bad enum");
+  if (objective > SDAS_MIN_P99_E2E_INTERACTIVE) return fail(SDAS_E_INVALID_ARG, "objective: bad enum");
   if (!dev || !dev->params || !dev->summary || !dev->best_group)
     return fail(SDAS_E_BUFFER, "group_argmin needs params, summary and best_group");
   Plan pl;
@@ -595,7 +614,7 @@ sdas_status sdas_group_argmin(const sdas_pipeline* p, const sdas_grid* grid, uin
 
 sdas_status sdas_finalize(const sdas_pipeline* p, const sdas_grid* grid, uint32_t objective, uint64_t objective_slo,
                           const sdas_buffers* dev, void* stream) {
-  if (objective > SDAS_MIN_P90_E2E) return fail(SDAS_E_INVALID_ARG, "objective: bad enum");
+  if (objective > SDAS_MIN_P99_E2E_INTERACTIVE) return fail(SDAS_E_INVALID_ARG, "objective: bad enum");
   if (!dev || !dev->params || !dev->work || !dev->cell_cnt || !dev->cell_hist || !dev->best_row)
     return fail(SDAS_E_BUFFER, "finalize needs params, work, cell_cnt, cell_hist and best_row");
   Plan pl;
@@ -705,6 +724,8 @@ sdas_status sdas_metrics(const sdas_pipeline* p, const sdas_grid* grid, const sd
     out->arrivals = w[20]; out->deliveries = w[21]; out->recv_steps = w[22]; out->decode_steps = w[23];
     out->window_closes = w[24]; out->mode_switches = w[25]; out->good = w[26]; out->large_items = w[27];
     out->tokens = u64(28);
+    out->completed_int = w[32]; out->rejected = w[33]; out->sum_e2e_int = u64(34);
+    out->p50_e2e_int = w[36]; out->p99_e2e_int = w[37]; out->good_int = w[38];
     derive();
     if (host->series && (grid->flags & SDAS_FLAG_SERIES) && grid->series_stride) {
       const uint64_t lg = index / pl.hp.C, c = index % pl.hp.C;
@@ -721,7 +742,7 @@ sdas_status sdas_metrics(const sdas_pipeline* p, const sdas_grid* grid, const sd
     if (!host->cell_cnt || !host->cell_hist) return fail(SDAS_E_STATE, "CELL scope needs cell_cnt and cell_hist");
     if (index >= pl.n_cells) return fail(SDAS_E_INVALID_ARG, "index out of range");
     const int64_t* q = reinterpret_cast<const int64_t*>(host->cell_cnt) + index * SDAS_NCNT;
-    const int32_t* h = reinterpret_cast<const int32_t*>(host->cell_hist) + index * 2 * SDAS_NBINS;
+    const int32_t* h = reinterpret_cast<const int32_t*>(host->cell_hist) + index * SDAS_NHIST * SDAS_NBINS;
     out->status = q[1] == q[0] ? SDAS_REPLICA_OK : SDAS_REPLICA_OVERFLOW;
     out->n_replicas = q[0]; out->admitted = q[4]; out->dropped = q[5]; out->completed = q[6];
     out->sum_e2e = q[7]; out->sum_ff = q[8]; out->makespan = q[9]; out->int_nsys = q[10]; out->good = q[11];
@@ -746,8 +767,11 @@ sdas_status sdas_metrics(const sdas_pipeline* p, const sdas_grid* grid, const sd
     };
     pct(h, 50, &out->p50_e2e, &out->bin_p50_e2e);
     pct(h, 99, &out->p99_e2e, &out->bin_p99_e2e);
-    uint32_t bin90;
+    uint32_t bin90, binx;
     pct(h, 90, &out->p90_e2e, &bin90);
+    pct(h + 2 * SDAS_NBINS, 50, &out->p50_e2e_int, &binx);
+    pct(h + 2 * SDAS_NBINS, 99, &out->p99_e2e_int, &binx);
+    out->completed_int = q[24]; out->rejected = q[25]; out->sum_e2e_int = q[26]; out->good_int = q[27];
     pct(h + SDAS_NBINS, 50, &out->p50_ff, &out->bin_p50_ff);
     pct(h + SDAS_NBINS, 99, &out->p99_ff, &out->bin_p99_ff);
     derive();

@@ -11,7 +11,7 @@ namespace sdas {
 
 constexpr uint32_t kUnsetFF = 0xFFFFFFFFu;   // ff latency not yet observed (also "saturated")
 constexpr uint32_t kNever = 0xFFFFFFFFu;
-constexpr int kScratchMin = 2 * SDAS_NBINS * 4 + 256 * 4 + 128 + SDAS_NCNT * 8;  // finalize scratch
+constexpr int kScratchMin = SDAS_NHIST * SDAS_NBINS * 4 + 256 * 4 + 160 + SDAS_NCNT * 8;  // finalize scratch
 
 struct DInst {          // one instance, 64 B
   uint32_t role, h, alpha, beta, tau0, gamma, B_default, flags;   // flags: bit0 large, bit1 svc_exp
@@ -31,7 +31,7 @@ struct DLink {          // one link, 32 B
   uint32_t src, dst, net, chunk, mode, pad0, pad1, pad2;
 };
 
-struct DCand {          // one candidate, 64 B
+struct DCand {          // one candidate, 80 B
   uint32_t adaptive;
   uint8_t mode[8];
   uint32_t ctl_links, metric_load, lo, hi, dwell;
@@ -40,13 +40,18 @@ struct DCand {          // one candidate, 64 B
   int32_t select_role;
   uint8_t kv_policy, guard_links, guard_pct, pad0;   // guard: M25 (f3)
   uint64_t policy_slo;
+  uint32_t prio, admit;                              // f2: M27 priority service, M28 admission gate
+  uint16_t admit_lo, admit_hi;
+  uint32_t pad1;
 };
 
-struct DArr {           // one arrival descriptor, 64 B
+struct DArr {           // one arrival descriptor, 80 B
   uint32_t kind, list_len;
   uint64_t gap0, gap1, soj0, soj1;
   uint64_t list_off;    // byte offset of the LIST ticks inside the params blob
   uint32_t p_lo, p_hi, o_lo, o_hi;
+  uint64_t ithr;        // M26: interactive iff ATTR(sub 1).w0 < ithr = floor(permille * 2^32 / 1000)
+  uint64_t pad;
 };
 
 struct alignas(16) DParams {
@@ -58,6 +63,8 @@ struct alignas(16) DParams {
   uint32_t off_warps;        // byte offset of warp 0's region in the CTA's shared memory
   uint32_t off_reqA, off_reqFF, off_reqJ, off_reqO, off_reqNit, off_reqOut, off_bitmap, off_scratch;
   uint32_t max_out, need_lint, kv_role, kv_ctx, kv_tau, off_reqHome;
+  uint32_t cls, off_reqCls;   // f2: two request classes (class-1 rings follow the class-0 rings)
+  uint64_t off_rec_cls;       // f2: byte offset in `work` of the per-warp record-class arrays
   uint64_t kv_skew32;         // M21: home = instance 0 iff ATTR.w2 < kv_skew32 = floor(skew * 2^32 / 1000)
   uint64_t window, slo, max_ticks, master_seed;
   uint64_t first_group, n_local_groups, n_local_replicas, trace_replica;
@@ -69,8 +76,8 @@ struct alignas(16) DParams {
 
 static_assert(sizeof(DInst) == 64, "DInst");
 static_assert(sizeof(DRole) == 64, "DRole");
-static_assert(sizeof(DCand) == 64, "DCand");
-static_assert(sizeof(DArr) == 64, "DArr");
+static_assert(sizeof(DCand) == 80, "DCand");
+static_assert(sizeof(DArr) == 80, "DArr");
 static_assert(sizeof(DParams) % 16 == 0, "DParams");
 
 struct Work {              // head of the `work` buffer
@@ -86,7 +93,7 @@ int launch_group_argmin(const uint8_t* params_dev, const DParams& hp, const sdas
                         uint64_t slo, void* stream);
 int launch_finalize(const uint8_t* params_dev, const DParams& hp, const sdas_buffers* b, uint32_t objective,
                     uint64_t slo, uint64_t n_cells, uint64_t n_rows, void* stream);
-int query_occupancy(uint32_t warps_per_block, uint32_t smem_bytes, uint32_t maxout, int* blocks_per_sm,
+int query_occupancy(uint32_t warps_per_block, uint32_t smem_bytes, uint32_t maxout, uint32_t cls, int* blocks_per_sm,
                     int* n_sm);
 const char* cuda_error_string(int code);
 

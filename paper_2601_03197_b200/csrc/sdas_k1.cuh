@@ -10,9 +10,12 @@
 //     ballot/popc message placement, stable compaction;
 //   * shared memory: request table, per-instance rings (inbox, in-flight, decode-wait), batch words,
 //     controller state; the finalize scratch aliases the (dead) request table.
-// TRACE adds the debug event trace (separate instantiation); MAXOUT is the largest fan-out (1 or 2).
+// TRACE adds the debug event trace (separate instantiation); MAXOUT is the largest fan-out (1 or 2);
+// CLS (f2, M26-M29): two request classes -- per-class inbox / wait rings (class-1 ring right after the
+// class-0 ring; used only under priority service, so FIFO across classes holds otherwise), the
+// admission gate, per-class metrics.  Pipelines without interactive requests never pay for it.
 
-template <bool TRACE, int MAXOUT>
+template <bool TRACE, int MAXOUT, bool CLS>
 __global__ void __launch_bounds__(256, 2)
 k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* __restrict__ summary,
             unsigned long long* __restrict__ records_out, uint8_t* __restrict__ series,
@@ -68,6 +71,8 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
   const uint32_t my_hint_off =
       my_kv ? P.kv_tau * P.kv_ctx - P.link[P.role[kv_role].in_link].net : 0u;   // ready = delivery + this
   uint8_t* const rHome = Wr + P.off_reqHome;
+  uint8_t* const rCls = Wr + P.off_reqCls;                        // f2: class per request slot
+  uint8_t* const rec_cls = reinterpret_cast<uint8_t*>(work) + P.off_rec_cls + gwarp * N;
 
   for (;;) {
     unsigned long long x = 0;
@@ -116,6 +121,12 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
     // at the first step boundary >= its tick (RECV-first START, M7); flushm > 0 = a cut landed exactly
     // on a boundary of this tick and that many silent steps are applied before phase START.
     uint32_t runm = 1, flushm = 0;
+    // f2: class-1 (interactive) ring heads and counts; `in` / `wn` stay the totals over both rings
+    uint32_t ih1 = 0, in1 = 0, wh1 = 0, wn1 = 0;
+    const bool prio = CLS && cd.prio != 0;
+    uint32_t C_next = 0;                                  // class of the next arriving request (M26)
+    bool gate = false;                                    // M28: admission is interactive-only
+    int32_t q_last_gate = -(1 << 30);
 
     // uniform replica state
     unsigned long long t = 0, A_next = 0, int_nsys = 0;
@@ -193,6 +204,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
       P_next = uni(ad.p_lo, ad.p_hi, w.x);
       O_next = uni(ad.o_lo, ad.o_hi, w.y);
       if (kv_role) H_next = (unsigned long long)w.z < P.kv_skew32 ? 0u : uni(0u, P.role[kv_role].n - 1u, w.w);
+      if (CLS) C_next = (unsigned long long)philox(j, s_coord, 2u << 16, 1u, key0, key1).x < ad.ithr ? 1u : 0u;
       arr_near = A_next - t < 0x80000000ull;
       A_lo = (uint32_t)A_next;
     };
@@ -266,6 +278,15 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
         WarpHdr& h = *H;
         if (e2e >= 0xFFFFFFFFull || f32 == 0xFFFFFFFFu) ++h.n_sat;
         rec[h.completed] = (unsigned long long)e32 | ((unsigned long long)f32 << 32);
+        if (CLS) {                         // M29 per-class metrics
+          const uint32_t ci = rCls[slot];
+          rec_cls[h.completed] = (uint8_t)ci;
+          if (ci) {
+            ++h.completed_int;
+            h.sum_e2e_int += e2e;
+            h.good_int += e2e <= P.slo ? 1u : 0u;
+          }
+        }
         ++h.completed;
         h.sum_e2e += e2e;
         h.sum_ff += f32;
@@ -323,8 +344,15 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
           ovf = true;
           return;
         }
-        const uint32_t idx = wrap_add(__shfl_sync(FULL, wh, i), wn_i, I.wait_cap);
-        if (lane == 0) at<uint32_t>(Wr, I.off_wait)[idx] = slot | (out << 16);
+        if (CLS && prio && rCls[slot]) {   // M27: interactive items wait in the class-1 ring
+          const uint32_t idx = wrap_add(__shfl_sync(FULL, wh1, i), __shfl_sync(FULL, wn1, i), I.wait_cap);
+          if (lane == 0) at<uint32_t>(Wr, I.off_wait)[I.wait_cap + idx] = slot | (out << 16);
+          if (lane == (int)i) ++wn1;
+        } else {
+          const uint32_t idx = wrap_add(__shfl_sync(FULL, wh, i), wn_i - (CLS ? __shfl_sync(FULL, wn1, i) : 0u),
+                                        I.wait_cap);
+          if (lane == 0) at<uint32_t>(Wr, I.off_wait)[idx] = slot | (out << 16);
+        }
         if (lane == (int)i) ++wn;
         if (TRACE) trace(TR_ITEM_WAIT, i, rJ[slot], out);
         return;
@@ -515,7 +543,9 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
       __syncwarp();                       // rNit / rJ written by other lanes earlier in this tick
       uint32_t cost32 = 0, slot = 0;
       if (lane == (int)i) {
-        const unsigned long long body = reinterpret_cast<unsigned long long*>(my_inbox)[ih];
+        const bool from1 = CLS && in1 != 0u;                  // M27: interactive messages first
+        const unsigned long long body =
+            reinterpret_cast<unsigned long long*>(my_inbox)[from1 ? my_inbox_cap + ih1 : ih];
         slot = (uint32_t)(body & 0xFFFFu);
         const uint32_t flags = (uint32_t)(body >> 16) & 0xFFu;
         const uint32_t tokens = (uint32_t)(body >> 32) & 0xFFFFu;
@@ -544,7 +574,12 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
         st = RECV;
         end_lo = t_lo + cost32;
         cur = body;
-        ih = wrap_add(ih, 1u, my_inbox_cap);
+        if (from1) {
+          ih1 = wrap_add(ih1, 1u, my_inbox_cap);
+          --in1;
+        } else {
+          ih = wrap_add(ih, 1u, my_inbox_cap);
+        }
         --in;
       }
       if (TRACE) trace(TR_RECV_START, i, rJ[__shfl_sync(FULL, slot, i)], __shfl_sync(FULL, cost32, i));
@@ -558,10 +593,19 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
       const uint32_t n_out = R.n_out;
       uint32_t* const bat = at<uint32_t>(Wr, I.off_batch);
       uint32_t wA = 0, wB = 0, wD = 0;
+      uint32_t n1 = 0;                                    // admitted from the class-1 ring (M27)
       if (nadm) {
         const uint32_t wh_i = __shfl_sync(FULL, wh, i);
+        uint32_t wh1_i = 0;
+        if (CLS) {
+          n1 = min(nadm, __shfl_sync(FULL, wn1, i));
+          wh1_i = __shfl_sync(FULL, wh1, i);
+        }
         if (lane >= (int)bi && lane < (int)(bi + nadm)) {
-          const uint32_t e = at<uint32_t>(Wr, I.off_wait)[wrap_add(wh_i, lane - bi, I.wait_cap)];
+          const uint32_t k = lane - bi;
+          const uint32_t* const wr = at<uint32_t>(Wr, I.off_wait);
+          const uint32_t e = (CLS && k < n1) ? wr[I.wait_cap + wrap_add(wh1_i, k, I.wait_cap)]
+                                             : wr[wrap_add(wh_i, k - n1, I.wait_cap)];
           const uint32_t out = e >> 16;
           wA = (e & 0xFFFu) | (out << 16);
           for (uint32_t q = 0; q < n_out; ++q) {
@@ -615,8 +659,12 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
             m = (uint32_t)max(1ull, (max_ticks - min(t, max_ticks)) / cost32);
         }
       }
-      wh = me ? wrap_add(wh, nadm, my_wait_cap) : wh;
+      wh = me ? wrap_add(wh, nadm - n1, my_wait_cap) : wh;
       wn = me ? wn - nadm : wn;
+      if (CLS) {
+        wh1 = me ? wrap_add(wh1, n1, my_wait_cap) : wh1;
+        wn1 = me ? wn1 - n1 : wn1;
+      }
       b = me ? nbat : b;
       const bool go = me && nbat > 0;
       st = go ? (uint32_t)DECODE : st;
@@ -644,7 +692,13 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
     // ---------------------------------------------------------------- phase ARRIVE (M14)
     auto arrive = [&]() {
       const uint32_t j = jn;
-      if (nsys >= R_cap) {
+      if (CLS && gate && !C_next) {       // M28: interactive-only admission rejects a background request
+        if (lane == 0) {
+          ++H->dropped;
+          ++H->rejected;
+        }
+        if (TRACE) trace(TR_ARRIVE, j, 2, 0xFFFFFFFFu);
+      } else if (nsys >= R_cap) {
         if (lane == 0) ++H->dropped;
         if (TRACE) trace(TR_ARRIVE, j, 0, 0xFFFFFFFFu);
       } else {
@@ -667,13 +721,20 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
           rNit[slot] = 0;
           rOut[slot] = (uint16_t)O_next;
           rHome[slot] = (uint8_t)H_next;
+          if (CLS) rCls[slot] = (uint8_t)C_next;
         }
         const uint32_t dest = route(0, slot);
         if (TRACE) trace(TR_ARRIVE, j, 1, dest);
         const bool bad = lane == (int)dest && in >= my_inbox_cap;
         if (lane == (int)dest && !bad) {
-          reinterpret_cast<unsigned long long*>(my_inbox)[wrap_add(ih, in, my_inbox_cap)] =
-              make_body(slot, F_OPENS | F_CLOSES, P_next, P_next);
+          unsigned long long* const ib = reinterpret_cast<unsigned long long*>(my_inbox);
+          const unsigned long long body = make_body(slot, F_OPENS | F_CLOSES, P_next, P_next);
+          if (CLS && prio && C_next) {      // M27: class-1 ring
+            ib[my_inbox_cap + wrap_add(ih1, in1, my_inbox_cap)] = body;
+            ++in1;
+          } else {
+            ib[wrap_add(ih, in - (CLS ? in1 : 0u), my_inbox_cap)] = body;
+          }
           ++in;
           if (coalesce) cut_run();
         }
@@ -749,6 +810,20 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
             chm &= chm - 1;
             trace(TR_CONTROL, 1, k, __shfl_sync(FULL, Bk, k));
           }
+        }
+      }
+      if (CLS && cd.admit) {  // (iv) M28 admission gate on the source role's busy time
+        const DRole& R0 = P.role[0];
+        const bool mine = lane >= (int)R0.first && lane < (int)(R0.first + R0.n);
+        const unsigned long long u1000 = warp_sum64(mine ? (unsigned long long)acc_busy : 0ull) * 1000ull;
+        bool want = gate;
+        if (u1000 >= (unsigned long long)cd.admit_hi * P.window * R0.n) want = true;
+        else if (u1000 <= (unsigned long long)cd.admit_lo * P.window * R0.n) want = false;
+        if (want != gate && q - q_last_gate >= (int32_t)cd.dwell) {
+          gate = want;
+          q_last_gate = q;
+          if (lane == 0) ++H->gate_changes;
+          if (TRACE) trace(TR_CONTROL, 3, 0, want ? 1u : 0u);
         }
       }
       if (cd.select_role >= 0) {  // (iii) model selection
@@ -848,9 +923,14 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
           for (;;) {
             if (in >= my_inbox_cap) { lovf = true; break; }
             const unsigned long long body = fb[fh];
-            const uint32_t at_idx = wrap_add(ih, in, my_inbox_cap);
-            ib[at_idx] = body;
-            if (my_kv) my_iready[at_idx] = fhead + my_hint_off;   // emission + tau*ctx (M23 HINT)
+            if (CLS && prio && rCls[body & 0xFFFFu]) {        // M27: class-1 ring
+              ib[my_inbox_cap + wrap_add(ih1, in1, my_inbox_cap)] = body;
+              ++in1;
+            } else {
+              const uint32_t at_idx = wrap_add(ih, in - (CLS ? in1 : 0u), my_inbox_cap);
+              ib[at_idx] = body;
+              if (my_kv) my_iready[at_idx] = fhead + my_hint_off;   // emission + tau*ctx (M23 HINT)
+            }
             ++in;
             fh = wrap_add(fh, 1u, my_flight_cap);
             --fn;
@@ -915,11 +995,12 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
     uint8_t* const sum_out = summary + x * SDAS_SUMMARY_BYTES;
     const unsigned long long rid = g * C + c;
     const unsigned long long cell = ((g / P.S) % (P.I * (unsigned long long)P.K)) * C + c;
-    uint32_t* const stg = scratch + 2 * SDAS_NBINS + 256;
-    unsigned long long* const cst = reinterpret_cast<unsigned long long*>(stg + 32);
+    uint32_t* const stg = scratch + SDAS_NHIST * SDAS_NBINS + 256;   // 40 summary words, then counters
+    unsigned long long* const cst = reinterpret_cast<unsigned long long*>(stg + 40);
     __syncwarp();
     if (ovf) {
       stg[lane] = 0;
+      if (lane < 8) stg[32 + lane] = 0;
       __syncwarp();
       if (lane == 0) {
         stg[0] = SDAS_REPLICA_OVERFLOW;
@@ -927,10 +1008,11 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
         stg[5] = (uint32_t)(t >> 32);
         stg[12] = stg[13] = stg[14] = stg[15] = 0xFFFFFFFFu;
         stg[16] = stg[17] = 0xFFFFFFFFu;
-        stg[31] = 0;
+        stg[36] = stg[37] = 0xFFFFFFFFu;
       }
       __syncwarp();
-      if (lane < 8) reinterpret_cast<uint4*>(sum_out)[lane] = reinterpret_cast<const uint4*>(stg)[lane];
+      if (lane < SDAS_SUMMARY_BYTES / 16)
+        reinterpret_cast<uint4*>(sum_out)[lane] = reinterpret_cast<const uint4*>(stg)[lane];
       if (lane == 0) {
         atomicAdd(reinterpret_cast<unsigned long long*>(cell_cnt + cell * SDAS_NCNT + 0), 1ull);
         atomicAdd(reinterpret_cast<unsigned long long*>(cell_cnt + cell * SDAS_NCNT + 2), 1ull);
@@ -943,17 +1025,19 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
     const uint32_t completed = H->completed;
     uint32_t* const he = scratch;
     uint32_t* const hf = scratch + SDAS_NBINS;
-    uint32_t* const cnt = scratch + 2 * SDAS_NBINS;
-    for (uint32_t k = lane; k < 2 * SDAS_NBINS; k += 32) he[k] = 0;
+    uint32_t* const hi = scratch + 2 * SDAS_NBINS;       // interactive e2e (M29)
+    uint32_t* const cnt = scratch + SDAS_NHIST * SDAS_NBINS;
+    for (uint32_t k = lane; k < SDAS_NHIST * SDAS_NBINS; k += 32) he[k] = 0;
     __syncwarp();
     for (uint32_t k = lane; k < completed; k += 32) {  // log-bin histograms in shared memory (M17)
       const unsigned long long v = rec[k];
       atomicAdd(&he[bin_of((uint32_t)v)], 1u);
       atomicAdd(&hf[bin_of((uint32_t)(v >> 32))], 1u);
+      if (CLS && rec_cls[k]) atomicAdd(&hi[bin_of((uint32_t)v)], 1u);
     }
     __syncwarp();
     // exact nearest-rank percentiles: the histogram locates the bin, a radix select inside it (M18)
-    auto select = [&](const uint32_t* h, int field, uint32_t kq, uint32_t& val, uint32_t& binq) {
+    auto select = [&](const uint32_t* h, int field, uint32_t kq, uint32_t& val, uint32_t& binq, bool only_int) {
       const uint32_t lo_b = lane * 15u, hi_b = min(lo_b + 15u, (uint32_t)SDAS_NBINS);
       uint32_t part = 0;
       for (uint32_t bb = lo_b; bb < hi_b; ++bb) part += h[bb];
@@ -980,7 +1064,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
           const unsigned long long v64 = rec[z];
           const uint32_t v = field ? (uint32_t)(v64 >> 32) : (uint32_t)v64;
           const uint32_t off = v - lo;
-          if (v >= lo && (off >> nbits) == 0u && (off >> (shift + db)) == prefix)
+          if (v >= lo && (off >> nbits) == 0u && (off >> (shift + db)) == prefix && (!only_int || rec_cls[z]))
             atomicAdd(&cnt[(off >> shift) & ((1u << db) - 1u)], 1u);
         }
         __syncwarp();
@@ -1008,11 +1092,17 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
     if (completed > 0) {
       const uint32_t k50 = (uint32_t)((50ull * completed + 99ull) / 100ull);
       const uint32_t k99 = (uint32_t)((99ull * completed + 99ull) / 100ull);
-      select(he, 0, k50, v50e, b50e);
-      select(he, 0, k99, v99e, b99e);
-      select(he, 0, (uint32_t)((90ull * completed + 99ull) / 100ull), v90e, b90e);
-      select(hf, 1, k50, v50f, b50f);
-      select(hf, 1, k99, v99f, b99f);
+      select(he, 0, k50, v50e, b50e, false);
+      select(he, 0, k99, v99e, b99e, false);
+      select(he, 0, (uint32_t)((90ull * completed + 99ull) / 100ull), v90e, b90e, false);
+      select(hf, 1, k50, v50f, b50f, false);
+      select(hf, 1, k99, v99f, b99f, false);
+    }
+    uint32_t v50i = 0xFFFFFFFFu, v99i = 0xFFFFFFFFu, bi_unused = 0;
+    const uint32_t n_int = CLS ? H->completed_int : 0u;
+    if (CLS && n_int > 0) {             // M29: exact percentiles over the interactive records alone
+      select(hi, 0, (uint32_t)((50ull * n_int + 99ull) / 100ull), v50i, bi_unused, true);
+      select(hi, 0, (uint32_t)((99ull * n_int + 99ull) / 100ull), v99i, bi_unused, true);
     }
     const uint32_t deliv = __reduce_add_sync(FULL, is_inst ? cnt_deliv : 0u);
     const uint32_t recvs = __reduce_add_sync(FULL, is_inst ? cnt_recv : 0u);
@@ -1041,6 +1131,10 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
       stg[28] = (uint32_t)tokens; stg[29] = (uint32_t)(tokens >> 32);
       stg[30] = (batch_changes & 0xFFFFu) | (select_changes << 16);
       stg[31] = kvs;
+      stg[32] = h.completed_int; stg[33] = h.rejected;
+      stg[34] = (uint32_t)h.sum_e2e_int; stg[35] = (uint32_t)(h.sum_e2e_int >> 32);
+      stg[36] = v50i; stg[37] = v99i; stg[38] = h.good_int; stg[39] = h.gate_changes;
+      cst[24] = h.completed_int; cst[25] = h.rejected; cst[26] = h.sum_e2e_int; cst[27] = h.good_int;
       cst[0] = 1; cst[1] = status == SDAS_REPLICA_OK; cst[2] = 0; cst[3] = status == SDAS_REPLICA_TRUNCATED;
       cst[4] = admitted; cst[5] = dropped; cst[6] = completed; cst[7] = sum_e2e; cst[8] = sum_ff;
       cst[9] = t; cst[10] = int_nsys; cst[11] = good; cst[12] = larges; cst[13] = arrivals;
@@ -1049,9 +1143,10 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
       cst[23] = kvs;
     }
     __syncwarp();
-    if (lane < 8) reinterpret_cast<uint4*>(sum_out)[lane] = reinterpret_cast<const uint4*>(stg)[lane];
-    int* const ch = cell_hist + cell * (2 * SDAS_NBINS);
-    for (uint32_t k = lane; k < 2 * SDAS_NBINS; k += 32) {
+    if (lane < SDAS_SUMMARY_BYTES / 16)
+      reinterpret_cast<uint4*>(sum_out)[lane] = reinterpret_cast<const uint4*>(stg)[lane];
+    int* const ch = cell_hist + cell * (SDAS_NHIST * SDAS_NBINS);
+    for (uint32_t k = lane; k < (CLS ? SDAS_NHIST : 2) * SDAS_NBINS; k += 32) {
       const uint32_t v = he[k];
       if (v) atomicAdd(ch + k, (int)v);
     }

@@ -36,11 +36,12 @@ struct SeriesRec { unsigned long long qint; uint32_t busy; uint16_t maxq; uint8_
 static_assert(sizeof(TraceRec) == 24 && sizeof(SeriesRec) == 16, "record sizes");
 
 struct WarpHdr {                        // per-replica counters owned by lane 0 (read by all after __syncwarp)
-  unsigned long long sum_e2e, sum_ff;
+  unsigned long long sum_e2e, sum_ff, sum_e2e_int;
   uint32_t admitted, dropped, completed, max_e2e;
   uint32_t n_sat, good, w_n, w_good;
   uint32_t w_half, window_closes, mode_switches, batch_changes;
-  uint32_t select_changes, pad0, pad1, pad2;
+  uint32_t select_changes, completed_int, rejected, good_int;   // f2 (M28, M29)
+  uint32_t gate_changes, pad0, pad1, pad2;
 };
 static_assert(sizeof(WarpHdr) <= 256, "WarpHdr");
 
@@ -166,6 +167,9 @@ __device__ bool better(const Key& a, const Key& b, uint32_t obj, unsigned long l
       return a.dropped < b.dropped;
     }
     if (a.p != b.p) return a.p < b.p;
+  } else if (obj == SDAS_MIN_P99_E2E_INTERACTIVE) {   // M29: interactive latency only
+    if (a.p != b.p) return a.p < b.p;
+    if (a.sum != b.sum) return a.sum < b.sum;
   } else {
     if (a.dropped != b.dropped) return a.dropped < b.dropped;
     if (a.p != b.p) return a.p < b.p;
@@ -215,9 +219,10 @@ __global__ void k3_group_argmin(const uint8_t* __restrict__ blob, const uint8_t*
     k.dropped = s[2];
     k.completed = s[3];
     k.makespan = s[4] | ((unsigned long long)s[5] << 32);
-    const bool ff = obj == SDAS_MIN_P99_FF;
-    k.sum = ff ? (s[8] | ((unsigned long long)s[9] << 32)) : (s[6] | ((unsigned long long)s[7] << 32));
-    k.p = obj == SDAS_MIN_P50_E2E ? s[12] : obj == SDAS_MIN_P90_E2E ? s[17] : (ff ? s[15] : s[13]);
+    const bool ff = obj == SDAS_MIN_P99_FF, in = obj == SDAS_MIN_P99_E2E_INTERACTIVE;
+    const int sw = ff ? 8 : in ? 34 : 6;
+    k.sum = s[sw] | ((unsigned long long)s[sw + 1] << 32);
+    k.p = obj == SDAS_MIN_P50_E2E ? s[12] : obj == SDAS_MIN_P90_E2E ? s[17] : ff ? s[15] : in ? s[37] : s[13];
     k.good = s[26];
     k.large = s[27];
     if (!have || better(k, bk, obj, slo)) { bk = k; have = true; }
@@ -232,7 +237,8 @@ __global__ void k4_cell_pct(const uint8_t* __restrict__ blob, const int* __restr
   const unsigned long long cell = (unsigned long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (cell >= n_cells) return;
-  const int* h = cell_hist + cell * (2 * SDAS_NBINS) + (obj == SDAS_MIN_P99_FF ? SDAS_NBINS : 0);
+  const int* h = cell_hist + cell * (SDAS_NHIST * SDAS_NBINS) +
+                 (obj == SDAS_MIN_P99_FF ? SDAS_NBINS : obj == SDAS_MIN_P99_E2E_INTERACTIVE ? 2 * SDAS_NBINS : 0);
   const uint32_t lo_b = lane * 15u, hi_b = min(lo_b + 15u, (uint32_t)SDAS_NBINS);
   unsigned long long part = 0;
   for (uint32_t b = lo_b; b < hi_b; ++b) part += (uint32_t)h[b];
@@ -278,7 +284,7 @@ __global__ void k5_row_argmin(const uint8_t* __restrict__ blob, const long long*
     k.c = c;
     k.dropped = (unsigned long long)q[5];
     k.p = cell_p[cell];
-    k.sum = (unsigned long long)(obj == SDAS_MIN_P99_FF ? q[8] : q[7]);
+    k.sum = (unsigned long long)(obj == SDAS_MIN_P99_FF ? q[8] : obj == SDAS_MIN_P99_E2E_INTERACTIVE ? q[26] : q[7]);
     k.completed = (unsigned long long)q[6];
     k.makespan = (unsigned long long)q[9];
     k.good = (unsigned long long)q[11];
@@ -292,15 +298,19 @@ __global__ void k5_row_argmin(const uint8_t* __restrict__ blob, const long long*
 // ------------------------------------------------------------------------------ launchers
 typedef void (*K1Fn)(const uint8_t*, Work*, uint8_t*, unsigned long long*, uint8_t*, long long*, int*, uint8_t*);
 
-static K1Fn k1_pick(bool trace, uint32_t maxout) {
-  if (maxout > 1) return trace ? k1_simulate<true, 2> : k1_simulate<false, 2>;
-  return trace ? k1_simulate<true, 1> : k1_simulate<false, 1>;
+static K1Fn k1_pick(bool trace, uint32_t maxout, bool cls) {
+  if (cls) {
+    if (maxout > 1) return trace ? k1_simulate<true, 2, true> : k1_simulate<false, 2, true>;
+    return trace ? k1_simulate<true, 1, true> : k1_simulate<false, 1, true>;
+  }
+  if (maxout > 1) return trace ? k1_simulate<true, 2, false> : k1_simulate<false, 2, false>;
+  return trace ? k1_simulate<true, 1, false> : k1_simulate<false, 1, false>;
 }
 
 int launch_simulate(const uint8_t* params_dev, const DParams& hp, const sdas_buffers* bf, uint32_t blocks,
                     uint32_t warps_per_block, uint32_t smem_bytes, void* stream, const uint64_t* log2_table) {
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  const K1Fn fn = k1_pick((hp.flags & SDAS_FLAG_TRACE) != 0, hp.max_out);
+  const K1Fn fn = k1_pick((hp.flags & SDAS_FLAG_TRACE) != 0, hp.max_out, hp.cls != 0);
   cudaError_t e = cudaMemcpyToSymbolAsync(c_log2, log2_table, sizeof(uint64_t) * 257, 0, cudaMemcpyHostToDevice, s);
   if (e != cudaSuccess) return (int)e;
   e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes);
@@ -355,14 +365,14 @@ int launch_finalize(const uint8_t* params_dev, const DParams& hp, const sdas_buf
   return (int)cudaGetLastError();
 }
 
-int query_occupancy(uint32_t warps_per_block, uint32_t smem_bytes, uint32_t maxout, int* blocks_per_sm,
+int query_occupancy(uint32_t warps_per_block, uint32_t smem_bytes, uint32_t maxout, uint32_t cls, int* blocks_per_sm,
                     int* n_sm) {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return (int)e;
   e = cudaDeviceGetAttribute(n_sm, cudaDevAttrMultiProcessorCount, dev);
   if (e != cudaSuccess) return (int)e;
-  const K1Fn fn = k1_pick(false, maxout);
+  const K1Fn fn = k1_pick(false, maxout, cls != 0);
   e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes);
   if (e != cudaSuccess) return (int)e;
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, fn, (int)warps_per_block * 32, smem_bytes);

@@ -25,7 +25,7 @@ def reduce_cells(result, group=None):
     import torch.distributed as dist
     L = result.layout
     cnt = result.t["cell_cnt"][: L.n_cells * sdas.NCNT * 8].view(dtype=__import__("torch").int64)
-    hist = result.t["cell_hist"][: L.n_cells * 2 * sdas.NBINS * 4].view(dtype=__import__("torch").int32)
+    hist = result.t["cell_hist"][: L.n_cells * sdas.NHIST * sdas.NBINS * 4].view(dtype=__import__("torch").int32)
     dist.all_reduce(cnt, op=dist.ReduceOp.SUM, group=group)
     dist.all_reduce(hist, op=dist.ReduceOp.SUM, group=group)
 

@@ -31,12 +31,12 @@ def _kv_fields(pipe):
 
 ARRIVALS = {"poisson": 0, "mmpp2": 1, "det": 2, "list": 3}
 OBJECTIVES = {"p99_e2e": 0, "p50_e2e": 1, "p99_ff": 2, "throughput": 3, "goodput": 4, "large_under_slo": 5,
-              "p90_e2e": 6}
+              "p90_e2e": 6, "p99_e2e_int": 7}
 INTENTS = {None: 0, "max_throughput": 1, "min_p90_latency": 2}
 CONSTRAINT_METRICS = {"e2e_p90": 0, "e2e_p99": 1}
 SCOPES = {"replica": 0, "cell": 1, "group": 2, "row": 3}
 FLAG_RECORDS, FLAG_SERIES, FLAG_TRACE, FLAG_STEPWISE = 1, 2, 4, 8
-NBINS, NCNT = 464, 24
+NBINS, NCNT, NHIST = 464, 28, 3
 ROUTE_NONE = 255
 
 SUMMARY_DTYPE = np.dtype([
@@ -46,14 +46,17 @@ SUMMARY_DTYPE = np.dtype([
     ("bin_p50_e2e", "<u2"), ("bin_p99_e2e", "<u2"), ("p90_e2e", "<u4"), ("max_e2e", "<u4"), ("n_saturated", "<u4"),
     ("arrivals", "<u4"), ("deliveries", "<u4"), ("recv_steps", "<u4"), ("decode_steps", "<u4"),
     ("window_closes", "<u4"), ("mode_switches", "<u4"), ("good", "<u4"), ("large_items", "<u4"),
-    ("tokens", "<u8"), ("batch_changes", "<u2"), ("select_changes", "<u2"), ("kv_transfers", "<u4")])
-assert SUMMARY_DTYPE.itemsize == 128
+    ("tokens", "<u8"), ("batch_changes", "<u2"), ("select_changes", "<u2"), ("kv_transfers", "<u4"),
+    ("completed_int", "<u4"), ("rejected", "<u4"), ("sum_e2e_int", "<u8"), ("p50_e2e_int", "<u4"),
+    ("p99_e2e_int", "<u4"), ("good_int", "<u4"), ("gate_changes", "<u4")])
+assert SUMMARY_DTYPE.itemsize == 160
 SERIES_DTYPE = np.dtype([("qint", "<u8"), ("busy", "<u4"), ("maxq", "<u2"), ("mode", "u1"), ("B", "u1")])
 TRACE_DTYPE = np.dtype([("tick", "<u8"), ("code", "<u4"), ("a", "<u4"), ("b", "<u4"), ("c", "<u4")])
 CELL_FIELDS = ["n_replicas", "n_ok", "n_overflow", "n_truncated", "admitted", "dropped", "completed",
                "sum_e2e", "sum_ff", "makespan_sum", "int_nsys", "good", "large_items", "arrivals",
                "deliveries", "recv_steps", "decode_steps", "window_closes", "mode_switches", "tokens",
-               "batch_changes", "select_changes", "n_saturated", "kv_transfers"]
+               "batch_changes", "select_changes", "n_saturated", "kv_transfers", "completed_int", "rejected",
+               "sum_e2e_int", "good_int"]
 
 
 class SdasError(RuntimeError):
@@ -91,7 +94,9 @@ class Candidate(C.Structure):
                 ("lo_permille", C.c_uint32), ("hi_permille", C.c_uint32), ("dwell_windows", C.c_uint32),
                 ("band_mode", C.c_uint8 * 4), ("route_override", C.c_uint32), ("batch_roles", C.c_uint32),
                 ("q_hi", C.c_uint32), ("select_role", C.c_int32), ("kv_policy", C.c_uint32),
-                ("guard_links", C.c_uint32), ("guard_pct", C.c_uint32), ("policy_slo_ticks", C.c_uint64)]
+                ("guard_links", C.c_uint32), ("guard_pct", C.c_uint32), ("prio", C.c_uint32), ("admit", C.c_uint32),
+                ("admit_lo_permille", C.c_uint32), ("admit_hi_permille", C.c_uint32),
+                ("policy_slo_ticks", C.c_uint64)]
 
 
 class Constraint(C.Structure):
@@ -106,7 +111,8 @@ class Intent(C.Structure):
 class ArrivalDesc(C.Structure):
     _fields_ = [("kind", C.c_uint32), ("mean_gap", C.c_uint64 * 2), ("mean_sojourn", C.c_uint64 * 2),
                 ("list", C.POINTER(C.c_uint64)), ("list_len", C.c_uint32), ("prompt_lo", C.c_uint32),
-                ("prompt_hi", C.c_uint32), ("out_lo", C.c_uint32), ("out_hi", C.c_uint32)]
+                ("prompt_hi", C.c_uint32), ("out_lo", C.c_uint32), ("out_hi", C.c_uint32),
+                ("interactive_permille", C.c_uint32)]
 
 
 class Grid(C.Structure):
@@ -145,7 +151,8 @@ class MetricsOut(C.Structure):
                 ("throughput", C.c_double), ("goodput", C.c_double)] + [
         (n, C.c_uint64) for n in ("makespan", "sum_e2e", "sum_ff", "int_nsys", "good", "large_items", "arrivals",
                                   "deliveries", "recv_steps", "decode_steps", "window_closes", "mode_switches",
-                                  "tokens", "message_events", "des_events")] + [
+                                  "tokens", "message_events", "des_events", "completed_int", "rejected",
+                                  "sum_e2e_int", "good_int")] + [("p50_e2e_int", C.c_uint32), ("p99_e2e_int", C.c_uint32),
         ("best", C.c_int32), ("series", C.c_void_p), ("series_len", C.c_uint64)]
 
 
@@ -223,6 +230,9 @@ def _candidate(c, n_links):
     x.kv_policy = KV_POLICIES[c.get("kv", "off")]
     x.guard_links = sum(1 << l for l in c.get("guard_links", ()))
     x.guard_pct = c.get("guard_pct", 90)
+    x.prio = 1 if c.get("prio") else 0
+    x.admit = 1 if c.get("admit") else 0
+    x.admit_lo_permille, x.admit_hi_permille = c.get("admit_band", (400, 800))
     return x
 
 
@@ -240,7 +250,8 @@ def _candidate_dict(x, n_links):
             "batch_roles": [r for r in range(32) if (x.batch_roles >> r) & 1], "q_hi": x.q_hi,
             "select_role": None if x.select_role < 0 else x.select_role, "policy_slo": x.policy_slo_ticks,
             "kv": kvinv[x.kv_policy], "guard_links": [l for l in range(n_links) if (x.guard_links >> l) & 1],
-            "guard_pct": x.guard_pct}
+            "guard_pct": x.guard_pct, "prio": bool(x.prio), "admit": bool(x.admit),
+            "admit_band": (x.admit_lo_permille, x.admit_hi_permille)}
 
 
 def compile_intent(pipeline, objective=None, constraints=(), rules=None):
@@ -285,6 +296,7 @@ class GridView:
                 A.list_len = len(a["list"])
             A.prompt_lo, A.prompt_hi = a["prompt"]
             A.out_lo, A.out_hi = a["output"]
+            A.interactive_permille = a.get("interactive", 0)
         if trace_replica is not None:
             flags |= FLAG_TRACE
         gb, ge = group_range if group_range is not None else (0, 0)
@@ -374,7 +386,7 @@ class Result:
 
     def summary(self):
         n = self.layout.n_local_replicas
-        raw = self.t["summary"][: n * 128].cpu().numpy()
+        raw = self.t["summary"][: n * SUMMARY_DTYPE.itemsize].cpu().numpy()
         return raw.view(SUMMARY_DTYPE)
 
     def records(self, N):
@@ -388,7 +400,7 @@ class Result:
     def cells(self):
         nc = self.layout.n_cells
         cnt = self.t["cell_cnt"][: nc * NCNT * 8].cpu().numpy().view(np.int64).reshape(nc, NCNT)
-        hist = self.t["cell_hist"][: nc * 2 * NBINS * 4].cpu().numpy().view(np.int32).reshape(nc, 2, NBINS)
+        hist = self.t["cell_hist"][: nc * NHIST * NBINS * 4].cpu().numpy().view(np.int32).reshape(nc, NHIST, NBINS)
         return cnt, hist
 
     def best_group(self):

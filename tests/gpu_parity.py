@@ -8,7 +8,8 @@ from paper_2601_03197_b200 import sdas
 FIELDS = ["status", "admitted", "dropped", "completed", "sum_e2e", "sum_ff", "int_nsys", "p50_e2e", "p99_e2e",
           "p50_ff", "p99_ff", "max_e2e", "n_saturated", "arrivals", "deliveries", "recv_steps", "decode_steps",
           "window_closes", "mode_switches", "good", "large_items", "tokens", "batch_changes", "select_changes",
-          "kv_transfers", "p90_e2e"]
+          "kv_transfers", "p90_e2e", "completed_int", "rejected", "sum_e2e_int", "p50_e2e_int", "p99_e2e_int",
+          "good_int", "gate_changes"]
 BINS = ["bin_p50_e2e", "bin_p99_e2e"]
 
 

@@ -232,3 +232,40 @@ def test_compiled_intent_grid(objective):
     gg, o = full_check(p, g, objective=objective)
     s = gg["summary"]
     assert s["mode_switches"].sum() > 0 and (s["p90_e2e"][s["status"] == 0] > 0).all()
+
+
+# ------------------------------------------------------------------ f2: classes, priority, admission (M26-M29)
+@pytest.mark.parametrize("prio", [False, True])
+def test_prio_single_server_trace(prio):
+    rng = np.random.default_rng(5)
+    ticks = np.cumsum(rng.integers(100, 1300, size=300)).tolist()
+    p = W.tool1(700)
+    g = W.grid([W.with_prio(W.static(), prio)], [W.with_classes(W.arr_list(ticks, prompt=(0, 0), output=(0, 0)),
+                                                                400)], n_requests=300)
+    gg, o = full_check(p, g)
+    tr = run_gpu(p, g, trace_replica=0)["trace"]
+    assert first_divergence(sorted_trace(tr), sorted_trace(oracle.simulate(p, g, trace_id=0)["trace"])) is None
+
+
+def test_config_prio_grid():
+    p, g = W.config_prio(n_seeds=3, n_requests=300, gaps=(1597600, 726182, 469882))
+    gg, o = full_check(p, g, objective="p99_e2e_int")
+    s = gg["summary"]
+    assert s["rejected"].sum() > 0 and s["gate_changes"].sum() > 0 and s["completed_int"].sum() > 0
+
+
+def test_prio_with_function_mode_jsq_and_controller():
+    # config-3 DAG (routing over 2 instances, SLO batch control) with classes and priority service
+    p, g = W.config3(n_seeds=2, n_requests=200)
+    g["arrivals"] = [[W.with_classes(a, 250) for a in row] for row in g["arrivals"]]
+    g["candidates"] = [W.with_prio(c, True, k % 2 == 1, (300, 700)) for k, c in enumerate(g["candidates"][:6])]
+    full_check(p, g, objective="p99_e2e_int")
+
+
+def test_prio_gate_window_series_and_stepwise():
+    p, g = W.config_prio(n_seeds=2, n_requests=300, gaps=(399400,))
+    g.update(series_stride=3, series_slots=6, series_windows=40)
+    full_check(p, g, series=True)
+    a = run_gpu(p, g, series=True)
+    b = run_gpu(p, g, series=True, stepwise=True)
+    assert a["summary"].tobytes() == b["summary"].tobytes()

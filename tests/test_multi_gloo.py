@@ -43,7 +43,7 @@ def _partial_cells(p, g, res, ids):
     """Cell sums over the given replicas (same counter layout as libsdas / oracle.cells)."""
     C, S, K, I = len(g["candidates"]), g["n_seeds"], len(g["arrivals"][0]), len(g["arrivals"])
     cnt = np.zeros((I * K * C, sdas.NCNT), np.int64)
-    hist = np.zeros((I * K * C, 2, sdas.NBINS), np.int64)
+    hist = np.zeros((I * K * C, sdas.NHIST, sdas.NBINS), np.int64)
     F = {n: i for i, n in enumerate(sdas.CELL_FIELDS)}
     for x, r in enumerate(ids):
         s = res["summary"][x]
@@ -57,7 +57,8 @@ def _partial_cells(p, g, res, ids):
         q[F["n_truncated"]] += s["status"] == 2
         for f in ("admitted", "dropped", "completed", "sum_e2e", "sum_ff", "int_nsys", "good", "large_items",
                   "arrivals", "deliveries", "recv_steps", "decode_steps", "window_closes", "mode_switches", "tokens",
-                  "batch_changes", "select_changes", "n_saturated"):
+                  "batch_changes", "select_changes", "n_saturated", "kv_transfers", "completed_int", "rejected",
+                  "sum_e2e_int", "good_int"):
             q[F[f]] += int(s[f])
         q[F["makespan_sum"]] += int(s["makespan"])
         hist[cell] += res["hists"][x]
