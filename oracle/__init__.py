@@ -79,7 +79,7 @@ class Role(C.Structure):
 
 
 class Link(C.Structure):
-    _fields_ = [(n, C.c_uint32) for n in ("src", "dst", "net", "chunk", "mode")]
+    _fields_ = [(n, C.c_uint32) for n in ("src", "dst", "net", "chunk", "mode", "pacing_gap")]
 
 
 class Arrival(C.Structure):
@@ -95,7 +95,8 @@ class Candidate(C.Structure):
                 ("band", C.c_uint32 * 3), ("route_override", C.c_uint32), ("batch_roles", C.c_uint32),
                 ("q_hi", C.c_uint32), ("select_role", C.c_int32), ("policy_slo", C.c_uint64),
                 ("kv_policy", C.c_uint32), ("guard_links", C.c_uint32), ("guard_pct", C.c_uint32),
-                ("prio", C.c_uint32), ("admit", C.c_uint32), ("admit_lo", C.c_uint32), ("admit_hi", C.c_uint32)]
+                ("prio", C.c_uint32), ("admit", C.c_uint32), ("admit_lo", C.c_uint32), ("admit_hi", C.c_uint32),
+                ("pacing_gap", C.c_uint32)]
 
 
 class Pipeline(C.Structure):
@@ -216,6 +217,7 @@ def _candidate(c, n_links):
     x.prio = 1 if c.get("prio") else 0
     x.admit = 1 if c.get("admit") else 0
     x.admit_lo, x.admit_hi = c.get("admit_band", (400, 800))
+    x.pacing_gap = 0xFFFFFFFF if c.get("pacing_gap") is None else int(c["pacing_gap"])
     return x
 
 
@@ -242,7 +244,7 @@ class Problem:
             R.inbox_cap, R.flight_cap, R.wait_cap = d["inbox_cap"], d["flight_cap"], d["wait_cap"]
         links = (Link * max(1, len(pipe["links"])))()
         for l, d in enumerate(pipe["links"]):
-            links[l] = Link(d["src"], d["dst"], d["net"], d["chunk"], MODES[d["mode"]])
+            links[l] = Link(d["src"], d["dst"], d["net"], d["chunk"], MODES[d["mode"]], d.get("pacing_gap", 0))
         self.pipe = Pipeline(len(pipe["roles"]), C.cast(roles, C.POINTER(Role)), len(pipe["links"]),
                              C.cast(links, C.POINTER(Link)), pipe["feedback_role"], pipe["request_cap"],
                              pipe["window"], pipe["slo"], *_kv(pipe))

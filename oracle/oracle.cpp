@@ -269,6 +269,7 @@ struct Replica {
   std::vector<int64_t> q_last_mode;
   std::vector<uint32_t> rr;                        // per role
   std::vector<uint32_t> sel;                       // per role
+  std::vector<uint64_t> pace_free;                 // M30: per link, earliest tick of the next dispatch
   int64_t q_last_sel = INT64_MIN / 2;
 
   std::vector<uint64_t> A;
@@ -343,7 +344,15 @@ struct Replica {
     inst[dest].inflight++;
     S.msgs_emitted++;
     S.tokens_emitted += tokens;
-    Event e{t + L.net, PH_DELIVER, ++seq, Msg{j, dest, l, opens, closes, tokens, n_in, kv_kind, ready}};
+    // M30 pacing ("consecutive emissions on one link are >= pacing_gap apart"): the message
+    // is dispatched at d = max(t, previous dispatch + gap) and arrives at d + net
+    const uint64_t gap = cand.pacing_gap == 0xFFFFFFFFu ? L.pacing_gap : cand.pacing_gap;
+    uint64_t d = t;
+    if (gap) {
+      d = std::max<uint64_t>(t, pace_free[l]);
+      pace_free[l] = d + gap;
+    }
+    Event e{d + L.net, PH_DELIVER, ++seq, Msg{j, dest, l, opens, closes, tokens, n_in, kv_kind, ready}};
     heap.push(e);
   }
 
@@ -708,6 +717,7 @@ struct Replica {
       cur_mode[l] = cand.mode[l] == 255 ? P.links[l].mode : cand.mode[l];
     base_mode = cur_mode;
     rr.assign(P.n_roles, 0);
+    pace_free.assign(P.n_links, 0);
     sel.resize(P.n_roles);
     for (uint32_t r = 0; r < P.n_roles; ++r) {
       sel[r] = role_first[r];

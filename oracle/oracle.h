@@ -42,7 +42,7 @@ typedef struct {
   uint32_t inbox_cap, flight_cap, wait_cap;
 } orc_role;
 
-typedef struct { uint32_t src, dst, net, chunk, mode; } orc_link;
+typedef struct { uint32_t src, dst, net, chunk, mode, pacing_gap; } orc_link;   /* pacing_gap: M30 (f4) */
 
 typedef struct {
   uint32_t kind;
@@ -70,6 +70,7 @@ typedef struct {
   uint32_t prio;                  /* M27 (f2): serve interactive first at every inbox and wait queue */
   uint32_t admit;                 /* M28 (f2): admission gate on the source role's busy fraction */
   uint32_t admit_lo, admit_hi;    /*   reopen at <= lo, interactive-only at >= hi (permille) */
+  uint32_t pacing_gap;            /* M30 (f4): 0xFFFFFFFF = each link's own gap, else this gap on every link */
 } orc_candidate;
 
 typedef struct {

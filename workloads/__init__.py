@@ -53,8 +53,8 @@ def role(name, n_instances=1, c=None, inst_cost=None, max_num_seqs=8, out=(0, 1,
             "inbox_cap": inbox_cap, "flight_cap": flight_cap, "wait_cap": wait_cap}
 
 
-def link(src, dst, net=1000, chunk=16, mode="batch"):
-    return {"src": src, "dst": dst, "net": net, "chunk": chunk, "mode": mode}
+def link(src, dst, net=1000, chunk=16, mode="batch", pacing_gap=0):
+    return {"src": src, "dst": dst, "net": net, "chunk": chunk, "mode": mode, "pacing_gap": pacing_gap}
 
 
 def pipeline(roles, links, feedback_role=None, request_cap=256, window=W_DEFAULT, slo=8_000_000):
@@ -366,3 +366,19 @@ def config_prio(n_seeds=8, n_requests=1000, interactive=300,
                 cands.append(with_prio(static(mode), prio, admit, (500, 850)))
     arrs = [with_classes(poisson(g), interactive) for g in gaps]
     return p2_x(), grid(cands, arrs, n_seeds=n_seeds, n_requests=n_requests)
+
+
+# ------------------------------------------------------------------ f4: data-plane pacing
+def with_pacing(cand, gap):
+    """Candidate that dispatches every link's messages at least `gap` ticks apart (M30)."""
+    c = copy.deepcopy(cand)
+    c["pacing_gap"] = int(gap)
+    return c
+
+
+def config_pace(n_seeds=8, n_requests=1000, gaps=(1597600, 726182, 469882),
+                pacing=(0, 2000, 8000, 20000)):
+    """f4 workload: P2-X with token streaming / per-function pipelining, swept over the link pacing gap
+    (PAPER.md:261 "priorities, and pacing strategies")."""
+    cands = [with_pacing(static(m), g) for m in ("token", "function", "batch") for g in pacing]
+    return p2_x(), grid(cands, [poisson(m) for m in gaps], n_seeds=n_seeds, n_requests=n_requests)
