@@ -107,6 +107,9 @@ typedef struct {
   uint32_t net_delay;          /* >= 1 tick; delivery = emit + net_delay */
   uint32_t chunk_tokens;       /* >= 1; TOKEN(c) chunk; knob "link:<s>-><d>/chunk_tokens" */
   uint32_t mode;               /* default granularity; knob "link:<s>-><d>/comm_mode" */
+  uint32_t pacing_gap;         /* M30 (f4): 0..2^18 ticks between consecutive dispatches on this link
+                                  (PAPER.md:261); knob "link:<s>-><d>/pacing_gap";
+                                  pacing_gap * the destination's flight_cap must stay below 2^30 */
 } sdas_link_desc;
 
 typedef struct {
@@ -139,6 +142,7 @@ void sdas_pipeline_destroy(sdas_pipeline* p); /* NULL-safe */
  *   "link:<src>-><dst>/comm_mode"    0..2       (SDAS_BATCH/FUNCTION/TOKEN)
  *   "link:<src>-><dst>/chunk_tokens" 1..65535
  *   "link:<src>-><dst>/net_delay"    1..2^31-1
+ *   "link:<src>-><dst>/pacing_gap"   0..2^18    (M30, f4)
  * Values set here are the initial knob values of every replica; reset restores the value given
  * at sdas_pipeline_create (idempotent).  Errors: SDAS_E_UNKNOWN_PARAM, SDAS_E_OUT_OF_RANGE. */
 sdas_status sdas_set(sdas_pipeline* p, const char* knob, int64_t value);
@@ -167,6 +171,8 @@ typedef struct {
   uint32_t admit;             /* M28 (f2): 1 = admission gate (agent-level rule "admit only high-priority
                                  requests under load"), needs ADAPTIVE */
   uint32_t admit_lo_permille, admit_hi_permille; /* gate opens at <= lo, interactive-only at >= hi */
+  uint32_t pacing_gap;        /* M30 (f4): 0xFFFFFFFF = every link's own pacing_gap knob; else this gap
+                                 (0..2^18 ticks) on every link */
   uint64_t policy_slo_ticks;  /* SLO used by the controller's window p99 test */
 } sdas_candidate;
 

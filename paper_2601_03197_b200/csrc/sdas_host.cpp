@@ -64,7 +64,7 @@ struct sdas_pipeline {
   uint32_t kv_role = 0, kv_ctx = 0, kv_tau = 0, kv_skew = 0;   // f1 (M21-M24)
   // knob registry: current values and registered defaults (Table 1)
   std::vector<uint32_t> B_cur, B_def, F_cur, F_def;
-  std::vector<uint32_t> mode_cur, mode_def, chunk_cur, chunk_def, net_cur, net_def;
+  std::vector<uint32_t> mode_cur, mode_def, chunk_cur, chunk_def, net_cur, net_def, pace_cur, pace_def;
   uint32_t n_inst = 0;
 };
 
@@ -128,6 +128,7 @@ sdas_status validate_desc(const sdas_pipeline_desc* d) {
       return fail(SDAS_E_INVALID_FIELD, "links[%u].net_delay: must be in 1..2^31-1", l);
     if (L.chunk_tokens < 1 || L.chunk_tokens > 65535)
       return fail(SDAS_E_INVALID_FIELD, "links[%u].chunk_tokens: must be in 1..65535", l);
+    if (L.pacing_gap > (1u << 18)) return fail(SDAS_E_INVALID_FIELD, "links[%u].pacing_gap: must be in 0..2^18", l);
     if (L.mode > SDAS_TOKEN) return fail(SDAS_E_INVALID_FIELD, "links[%u].mode: bad enum", l);
     indeg[L.dst_role]++;
     outdeg[L.src_role]++;
@@ -140,7 +141,8 @@ sdas_status validate_desc(const sdas_pipeline_desc* d) {
 }
 
 int parse_knob(const sdas_pipeline* p, const char* knob, int* kind, uint32_t* idx) {
-  // returns 0 ok; kinds: 0 max_num_seqs, 1 n_functions, 2 comm_mode, 3 chunk_tokens, 4 net_delay
+  // returns 0 ok; kinds: 0 max_num_seqs, 1 n_functions, 2 comm_mode, 3 chunk_tokens, 4 net_delay,
+  // 5 pacing_gap
   if (!knob) return -1;
   unsigned a = 0, b = 0;
   char name[64] = {0};
@@ -160,6 +162,7 @@ int parse_knob(const sdas_pipeline* p, const char* knob, int* kind, uint32_t* id
         if (!strcmp(name, "comm_mode")) { *kind = 2; return 0; }
         if (!strcmp(name, "chunk_tokens")) { *kind = 3; return 0; }
         if (!strcmp(name, "net_delay")) { *kind = 4; return 0; }
+        if (!strcmp(name, "pacing_gap")) { *kind = 5; return 0; }
         return -1;
       }
     }
@@ -287,12 +290,28 @@ sdas_status plan(const sdas_pipeline* p, const sdas_grid* g, Plan& pl) {
     const sdas_link_desc& L = p->links[l];
     DLink& D = h.link[l];
     D.src = L.src_role; D.dst = L.dst_role; D.net = p->net_cur[l]; D.chunk = p->chunk_cur[l]; D.mode = p->mode_cur[l];
+    D.gap = p->pace_cur[l];
     DRole& S = h.role[L.src_role];
     if (S.n_out == 0) S.out_link0 = l; else S.out_link1 = l;
     S.n_out++;
     h.role[L.dst_role].in_link = (int32_t)l;
   }
   h.kv_role = p->kv_role;
+  h.need_pace = 0;
+  for (uint32_t l = 0; l < nl; ++l) {
+    if (p->pace_cur[l] && (uint64_t)p->pace_cur[l] * p->roles[p->links[l].dst_role].flight_cap >= (1ull << 30))
+      return fail(SDAS_E_INVALID_FIELD, "links[%u]: pacing_gap x flight_cap must stay below 2^30", l);
+    if (p->pace_cur[l]) h.need_pace = 1;
+  }
+  for (uint32_t cc = 0; cc < g->n_candidates; ++cc) {
+    const uint32_t pg = g->cand[cc].pacing_gap;
+    if (pg == 0xFFFFFFFFu) continue;
+    if (pg > (1u << 18)) return fail(SDAS_E_INVALID_FIELD, "cand[%u].pacing_gap: 0..2^18 or 0xFFFFFFFF", cc);
+    for (uint32_t l = 0; l < nl && pg; ++l)
+      if ((uint64_t)pg * p->roles[p->links[l].dst_role].flight_cap >= (1ull << 30))
+        return fail(SDAS_E_INVALID_FIELD, "cand[%u].pacing_gap x flight_cap must stay below 2^30", cc);
+    if (pg) h.need_pace = 1;
+  }
   h.cls = 0;
   for (uint64_t a = 0; a < (uint64_t)g->n_rates * g->n_profiles; ++a)
     if (g->arrivals[a].interactive_permille) h.cls = 1;
@@ -409,6 +428,7 @@ void pack_blob(const sdas_grid* g, const Plan& pl, std::vector<uint8_t>& blob) {
     d.admit = s.admit ? 1u : 0u;
     d.admit_lo = (uint16_t)s.admit_lo_permille;
     d.admit_hi = (uint16_t)s.admit_hi_permille;
+    d.pace = s.pacing_gap;
   }
   const uint64_t nIK = (uint64_t)g->n_rates * g->n_profiles;
   DArr* da = reinterpret_cast<DArr*>(blob.data() + pl.hp.off_arr);
@@ -487,9 +507,10 @@ sdas_status sdas_pipeline_create(const sdas_pipeline_desc* desc, sdas_pipeline**
     p->mode_def.push_back(L.mode);
     p->chunk_def.push_back(L.chunk_tokens);
     p->net_def.push_back(L.net_delay);
+    p->pace_def.push_back(L.pacing_gap);
   }
   p->B_cur = p->B_def; p->F_cur = p->F_def;
-  p->mode_cur = p->mode_def; p->chunk_cur = p->chunk_def; p->net_cur = p->net_def;
+  p->mode_cur = p->mode_def; p->chunk_cur = p->chunk_def; p->net_cur = p->net_def; p->pace_cur = p->pace_def;
   p->feedback_role = desc->feedback_role;
   p->request_cap = desc->request_cap;
   p->window = desc->window_ticks;
@@ -509,12 +530,12 @@ sdas_status sdas_set(sdas_pipeline* p, const char* knob, int64_t value) {
   int kind;
   uint32_t idx;
   if (parse_knob(p, knob, &kind, &idx)) return fail(SDAS_E_UNKNOWN_PARAM, "unknown parameter '%s'", knob);
-  static const int64_t lo[5] = {1, 1, 0, 1, 1};
-  static const int64_t hi[5] = {SDAS_MAX_BATCH, 255, SDAS_TOKEN, 65535, (1ll << 31) - 1};
+  static const int64_t lo[6] = {1, 1, 0, 1, 1, 0};
+  static const int64_t hi[6] = {SDAS_MAX_BATCH, 255, SDAS_TOKEN, 65535, (1ll << 31) - 1, 1ll << 18};
   if (value < lo[kind] || value > hi[kind])
     return fail(SDAS_E_OUT_OF_RANGE, "value %lld out of range [%lld, %lld] for '%s'", (long long)value,
                 (long long)lo[kind], (long long)hi[kind], knob);
-  std::vector<uint32_t>* v[5] = {&p->B_cur, &p->F_cur, &p->mode_cur, &p->chunk_cur, &p->net_cur};
+  std::vector<uint32_t>* v[6] = {&p->B_cur, &p->F_cur, &p->mode_cur, &p->chunk_cur, &p->net_cur, &p->pace_cur};
   (*v[kind])[idx] = (uint32_t)value;
   return ok();
 }
@@ -524,8 +545,8 @@ sdas_status sdas_reset(sdas_pipeline* p, const char* knob) {
   int kind;
   uint32_t idx;
   if (parse_knob(p, knob, &kind, &idx)) return fail(SDAS_E_UNKNOWN_PARAM, "unknown parameter '%s'", knob);
-  std::vector<uint32_t>* cur[5] = {&p->B_cur, &p->F_cur, &p->mode_cur, &p->chunk_cur, &p->net_cur};
-  std::vector<uint32_t>* def[5] = {&p->B_def, &p->F_def, &p->mode_def, &p->chunk_def, &p->net_def};
+  std::vector<uint32_t>* cur[6] = {&p->B_cur, &p->F_cur, &p->mode_cur, &p->chunk_cur, &p->net_cur, &p->pace_cur};
+  std::vector<uint32_t>* def[6] = {&p->B_def, &p->F_def, &p->mode_def, &p->chunk_def, &p->net_def, &p->pace_def};
   (*cur[kind])[idx] = (*def[kind])[idx];
   return ok();
 }
@@ -535,7 +556,8 @@ sdas_status sdas_get(const sdas_pipeline* p, const char* knob, int64_t* value) {
   int kind;
   uint32_t idx;
   if (parse_knob(p, knob, &kind, &idx)) return fail(SDAS_E_UNKNOWN_PARAM, "unknown parameter '%s'", knob);
-  const std::vector<uint32_t>* cur[5] = {&p->B_cur, &p->F_cur, &p->mode_cur, &p->chunk_cur, &p->net_cur};
+  const std::vector<uint32_t>* cur[6] = {&p->B_cur, &p->F_cur, &p->mode_cur, &p->chunk_cur, &p->net_cur,
+                                         &p->pace_cur};
   *value = (*cur[kind])[idx];
   return ok();
 }
@@ -653,6 +675,7 @@ sdas_status sdas_compile_intent(const sdas_pipeline* p, const sdas_intent* in, s
     c.band_mode[3] = SDAS_BATCH;
     c.route_override = SDAS_ROUTE_NONE; c.q_hi = 2; c.select_role = -1; c.kv_policy = SDAS_KV_OFF;
     c.guard_pct = 90;
+    c.pacing_gap = 0xFFFFFFFFu;
   }
   uint32_t obj = SDAS_MIN_P99_E2E;
   const uint64_t W = p->window ? p->window : 1;

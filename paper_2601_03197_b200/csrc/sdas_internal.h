@@ -28,7 +28,7 @@ struct DRole {          // one role, 64 B
 };
 
 struct DLink {          // one link, 32 B
-  uint32_t src, dst, net, chunk, mode, pad0, pad1, pad2;
+  uint32_t src, dst, net, chunk, mode, gap, pad1, pad2;   // gap: M30 pacing (pipeline knob)
 };
 
 struct DCand {          // one candidate, 80 B
@@ -42,7 +42,7 @@ struct DCand {          // one candidate, 80 B
   uint64_t policy_slo;
   uint32_t prio, admit;                              // f2: M27 priority service, M28 admission gate
   uint16_t admit_lo, admit_hi;
-  uint32_t pad1;
+  uint32_t pace;                                     // f4 M30: 0xFFFFFFFF = link knobs, else every link
 };
 
 struct DArr {           // one arrival descriptor, 80 B
@@ -64,6 +64,7 @@ struct alignas(16) DParams {
   uint32_t off_reqA, off_reqFF, off_reqJ, off_reqO, off_reqNit, off_reqOut, off_bitmap, off_scratch;
   uint32_t max_out, need_lint, kv_role, kv_ctx, kv_tau, off_reqHome;
   uint32_t cls, off_reqCls;   // f2: two request classes (class-1 rings follow the class-0 rings)
+  uint32_t need_pace, pad_pace;   // f4: some link or candidate paces (M30)
   uint64_t off_rec_cls;       // f2: byte offset in `work` of the per-warp record-class arrays
   uint64_t kv_skew32;         // M21: home = instance 0 iff ATTR.w2 < kv_skew32 = floor(skew * 2^32 / 1000)
   uint64_t window, slo, max_ticks, master_seed;

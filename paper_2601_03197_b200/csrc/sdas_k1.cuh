@@ -48,6 +48,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
   const unsigned long long max_ticks = P.max_ticks;
   const bool need_lint = P.need_lint != 0;
   const bool coalesce = (P.flags & SDAS_FLAG_STEPWISE) == 0;   // silent DECODE runs
+  const bool need_pace = P.need_pace != 0;                     // f4 M30: some link is paced
   const uint32_t key0 = (uint32_t)P.master_seed, key1 = (uint32_t)(P.master_seed >> 32);
   const unsigned long long gwarp = (unsigned long long)blockIdx.x * (blockDim.x >> 5) + wib;
   unsigned long long* const rec_scratch =
@@ -244,6 +245,8 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
       return dest != P.role[kv_role].first + rHome[slot] ? cd.kv_policy : 0u;
     };
 
+    // M30 pacing gap of link l under this candidate (0 = unpaced)
+    auto pace_gap = [&](uint32_t l) -> uint32_t { return cd.pace == 0xFFFFFFFFu ? P.link[l].gap : cd.pace; };
     // one message into destination `dest`'s in-flight ring (uniform; used by the serial paths)
     auto push_msg = [&](uint32_t l, uint32_t dest, uint32_t slot, uint32_t tokens, uint32_t flags, uint32_t n_in) {
       const uint32_t net = P.link[l].net;
@@ -257,7 +260,19 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
         return;
       }
       const uint32_t idx = wrap_add(__shfl_sync(FULL, fh, dest), fn_d, D.flight_cap);
-      const uint32_t tick = t_lo + net;
+      uint32_t tick = t_lo + net;
+      if (need_pace) {                     // M30: dispatch at max(t, previous dispatch + gap)
+        const uint32_t gp = pace_gap(l);
+        if (gp) {
+          uint32_t tk = 0;
+          if (lane == 0) {
+            const unsigned long long d = max(t, H->pace_free[l]);
+            H->pace_free[l] = d + gp;
+            tk = (uint32_t)d + net;
+          }
+          tick = __shfl_sync(FULL, tk, 0);
+        }
+      }
       if (lane == 0) {
         at<uint32_t>(Wr, D.off_ftick)[idx] = tick;
         at<unsigned long long>(Wr, D.off_fbody)[idx] = make_body(slot, flags, tokens, n_in);
@@ -444,6 +459,15 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
             const uint32_t dest_single = Rd.first;
             uint32_t dest = (Rd.n == 1 || (flags & 1u)) ? dest_single : sticky;
             if (Rd.n == 1 && eq && (flags & 1u)) sticky = dest_single;
+            // M30 pacing: the link's messages of this step leave in batch order, gp apart
+            uint32_t gp = 0;
+            unsigned long long d0 = t;
+            if (need_pace) {
+              gp = pace_gap(l);
+              if (gp) d0 = max(t, H->pace_free[l]);
+            }
+            const uint32_t my_tick =
+                t_lo + P.link[l].net + (gp ? (uint32_t)(d0 - t) + (uint32_t)__popc(mq & lanemask_lt()) * gp : 0u);
             // group lanes by destination (continuations may target different instances)
             uint32_t todo = mq;
             while (todo) {
@@ -458,11 +482,11 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
                 ovf = true;
                 return;
               }
-              const uint32_t tick = t_lo + P.link[l].net;
+              const uint32_t tick = __shfl_sync(FULL, my_tick, __ffs(grp) - 1);   // group's first message
               if ((grp >> lane) & 1u) {
                 const uint32_t pos = __popc(grp & lanemask_lt());
                 const uint32_t idx = wrap_add(fh_d, fn_d + pos, D.flight_cap);
-                at<uint32_t>(Wr, D.off_ftick)[idx] = tick;
+                at<uint32_t>(Wr, D.off_ftick)[idx] = my_tick;
                 at<unsigned long long>(Wr, D.off_fbody)[idx] = make_body(slot, flags, tokens, n_in);
                 if (flags & 1u) atomicAdd(&rO[slot], 1u);          // M13: +1 per opening message
                 if (TRACE) trace_lane(TR_EMIT, dk, rJ[slot], tokens | ((flags & 1u) << 16) | (((flags >> 1) & 1u) << 17) | (l << 20));
@@ -473,6 +497,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
               }
             }
             __syncwarp();
+            if (gp && lane == 0) H->pace_free[l] = d0 + (unsigned long long)__popc(mq) * gp;
           } else {
             // openings need sequential routing (JSQ sees every earlier placement, M11)
             uint32_t todo = mq;

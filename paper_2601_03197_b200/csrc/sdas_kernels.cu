@@ -42,6 +42,7 @@ struct WarpHdr {                        // per-replica counters owned by lane 0 
   uint32_t w_half, window_closes, mode_switches, batch_changes;
   uint32_t select_changes, completed_int, rejected, good_int;   // f2 (M28, M29)
   uint32_t gate_changes, pad0, pad1, pad2;
+  unsigned long long pace_free[8];               // f4 M30: per link, earliest tick of the next dispatch
 };
 static_assert(sizeof(WarpHdr) <= 256, "WarpHdr");
 

@@ -79,7 +79,7 @@ class RoleDesc(C.Structure):
 
 
 class LinkDesc(C.Structure):
-    _fields_ = [(n, C.c_uint32) for n in ("src_role", "dst_role", "net_delay", "chunk_tokens", "mode")]
+    _fields_ = [(n, C.c_uint32) for n in ("src_role", "dst_role", "net_delay", "chunk_tokens", "mode", "pacing_gap")]
 
 
 class PipelineDesc(C.Structure):
@@ -95,7 +95,7 @@ class Candidate(C.Structure):
                 ("band_mode", C.c_uint8 * 4), ("route_override", C.c_uint32), ("batch_roles", C.c_uint32),
                 ("q_hi", C.c_uint32), ("select_role", C.c_int32), ("kv_policy", C.c_uint32),
                 ("guard_links", C.c_uint32), ("guard_pct", C.c_uint32), ("prio", C.c_uint32), ("admit", C.c_uint32),
-                ("admit_lo_permille", C.c_uint32), ("admit_hi_permille", C.c_uint32),
+                ("admit_lo_permille", C.c_uint32), ("admit_hi_permille", C.c_uint32), ("pacing_gap", C.c_uint32),
                 ("policy_slo_ticks", C.c_uint64)]
 
 
@@ -233,6 +233,7 @@ def _candidate(c, n_links):
     x.prio = 1 if c.get("prio") else 0
     x.admit = 1 if c.get("admit") else 0
     x.admit_lo_permille, x.admit_hi_permille = c.get("admit_band", (400, 800))
+    x.pacing_gap = 0xFFFFFFFF if c.get("pacing_gap") is None else int(c["pacing_gap"])
     return x
 
 
@@ -251,7 +252,8 @@ def _candidate_dict(x, n_links):
             "select_role": None if x.select_role < 0 else x.select_role, "policy_slo": x.policy_slo_ticks,
             "kv": kvinv[x.kv_policy], "guard_links": [l for l in range(n_links) if (x.guard_links >> l) & 1],
             "guard_pct": x.guard_pct, "prio": bool(x.prio), "admit": bool(x.admit),
-            "admit_band": (x.admit_lo_permille, x.admit_hi_permille)}
+            "admit_band": (x.admit_lo_permille, x.admit_hi_permille),
+            "pacing_gap": None if x.pacing_gap == 0xFFFFFFFF else x.pacing_gap}
 
 
 def compile_intent(pipeline, objective=None, constraints=(), rules=None):
@@ -338,7 +340,7 @@ class Pipeline:
             R.inbox_cap, R.flight_cap, R.wait_cap = d["inbox_cap"], d["flight_cap"], d["wait_cap"]
         links = (LinkDesc * max(1, len(pipe["links"])))()
         for l, d in enumerate(pipe["links"]):
-            links[l] = LinkDesc(d["src"], d["dst"], d["net"], d["chunk"], MODES[d["mode"]])
+            links[l] = LinkDesc(d["src"], d["dst"], d["net"], d["chunk"], MODES[d["mode"]], d.get("pacing_gap", 0))
         desc = PipelineDesc(len(pipe["roles"]), C.cast(roles, C.POINTER(RoleDesc)), len(pipe["links"]),
                             C.cast(links, C.POINTER(LinkDesc)), pipe["feedback_role"], pipe["request_cap"],
                             pipe["window"], pipe["slo"], *_kv_fields(pipe))

@@ -134,3 +134,15 @@ def test_simulate_without_gpu_fails_loudly():
     P = sdas.Pipeline(pipe)
     with pytest.raises(sdas.SdasError):
         sdas.simulate(P, sdas.GridView(pipe, g))
+
+
+def test_pacing_gap_knob():
+    P = sdas.Pipeline(W.p2_x())
+    assert P.get("link:0->1/pacing_gap") == 0
+    P.set("link:0->1/pacing_gap", 5000)
+    assert P.get("link:0->1/pacing_gap") == 5000
+    with pytest.raises(sdas.SdasError) as e:
+        P.set("link:0->1/pacing_gap", (1 << 18) + 1)
+    assert e.value.code == sdas.E_OUT_OF_RANGE
+    P.reset("link:0->1/pacing_gap")
+    assert P.get("link:0->1/pacing_gap") == 0

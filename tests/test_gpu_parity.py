@@ -269,3 +269,40 @@ def test_prio_gate_window_series_and_stepwise():
     a = run_gpu(p, g, series=True)
     b = run_gpu(p, g, series=True, stepwise=True)
     assert a["summary"].tobytes() == b["summary"].tobytes()
+
+
+# ------------------------------------------------------------------ f4: data-plane pacing (M30)
+def test_pacing_spec_example_trace():
+    p = W.toy_ht("batch")
+    p["links"][0].update(net=1, pacing_gap=5)
+    g = W.grid([W.static("batch")], [W.arr_list([0, 0], prompt=(4, 4), output=(1, 1))], n_requests=2)
+    full_check(p, g)
+    gg = run_gpu(p, g, trace_replica=0)
+    assert first_divergence(sorted_trace(gg["trace"]), sorted_trace(oracle.simulate(p, g, trace_id=0)["trace"])) is None
+
+
+@pytest.mark.parametrize("svc", ["det", "exp"])
+def test_paced_tandem(svc):
+    p = W.tandem(60000, 70000, 1000, svc=svc)
+    p["links"][0]["pacing_gap"] = 90000
+    g = W.grid([W.static("batch"), W.with_pacing(W.static("batch"), 50000), W.with_pacing(W.static("batch"), 0)],
+               [W.poisson(100000, output=(0, 0))], n_seeds=9, n_requests=700)
+    full_check(p, g)
+
+
+def test_config_pace_grid():
+    p, g = W.config_pace(n_seeds=3, n_requests=300)
+    gg, o = full_check(p, g, objective="p99_e2e")
+    a = run_gpu(p, g)
+    b = run_gpu(p, g, stepwise=True)
+    assert a["summary"].tobytes() == b["summary"].tobytes()
+
+
+def test_pacing_with_fanout_routing_and_classes():
+    # config-3 DAG: fan-out (MAXOUT 2), JSQ over two instances, paced links, and request classes
+    p, g = W.config3(n_seeds=2, n_requests=200)
+    for k, L in enumerate(p["links"]):
+        L["pacing_gap"] = 3000 * (k + 1)
+    g["arrivals"] = [[W.with_classes(a, 300) for a in row] for row in g["arrivals"]]
+    g["candidates"] = [W.with_prio(c, k % 2 == 0) for k, c in enumerate(g["candidates"][:6])]
+    full_check(p, g)
