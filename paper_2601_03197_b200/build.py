@@ -25,7 +25,8 @@ def build(force=False, verbose=False, debug=False, out=None):
     if not force and out == LIB and not needs_build():
         return LIB
     flags = [f for f in FLAGS if f not in ("-O3", "-lineinfo")] + ["-G"] if debug else FLAGS
-    cmd = [NVCC] + flags + (["-Xptxas", "-v"] if verbose else []) + ["-o", out] + SOURCES
+    extra = os.environ.get("SDAS_NVCC_EXTRA", "").split()   # experiments only (e.g. -DK1_LB_THREADS=128)
+    cmd = [NVCC] + flags + extra + (["-Xptxas", "-v"] if verbose else []) + ["-o", out] + SOURCES
     subprocess.check_call(cmd, cwd=HERE)
     return LIB
 

@@ -15,8 +15,12 @@
 // class-0 ring; used only under priority service, so FIFO across classes holds otherwise), the
 // admission gate, per-class metrics.  Pipelines without interactive requests never pay for it.
 
+#ifndef K1_LB_THREADS
+#define K1_LB_THREADS 256   // 2 x 8 warps per SM at <= 128 registers
+#define K1_LB_BLOCKS 2
+#endif
 template <bool TRACE, int MAXOUT, bool CLS>
-__global__ void __launch_bounds__(256, 2)
+__global__ void __launch_bounds__(K1_LB_THREADS, K1_LB_BLOCKS)
 k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* __restrict__ summary,
             unsigned long long* __restrict__ records_out, uint8_t* __restrict__ series,
             long long* __restrict__ cell_cnt, int* __restrict__ cell_hist, uint8_t* __restrict__ trace_buf) {
