@@ -267,10 +267,17 @@ def main():
     k1_avg_s = statistics.mean(k1_ms) / 1e3
     achieved = ALG_WARP_INSTR_PER_DES_EVENT * (loc_des / args.steps) / k1_avg_s / 1e12
     traffic = None
+    issue = None
     try:
         prof = json.load(open(os.path.join(ROOT, "profiles", "k1_ncu_summary.json")))
         if prof.get("dram_bytes_per_des_event") is not None:
             traffic = prof["dram_bytes_per_des_event"] * (loc_des / args.steps)
+        if prof.get("warp_instr_per_des_event") is not None:
+            # the same roofline with the ncu-MEASURED instructions per DES event (profiles/): issue utilisation
+            w = float(prof["warp_instr_per_des_event"])
+            issue = {"warp_instr_per_des_event": w,
+                     "achieved": w * (loc_des / args.steps) / k1_avg_s / 1e12,
+                     "frac": w * (loc_des / args.steps) / k1_avg_s / 1e12 / peak}
     except Exception:
         pass
 
@@ -322,7 +329,7 @@ def main():
             "phase_ms": {"k1_simulate": statistics.mean(k1_ms), "k3_group_argmin": statistics.mean(k3_ms),
                          "collective": statistics.mean(coll_ms), "k4k5_finalize": statistics.mean(fin_ms)},
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "warp-instr/s x1e12",
-                         "frac": achieved / peak, "traffic": traffic,
+                         "frac": achieved / peak, "traffic": traffic, "measured_issue": issue,
                          "note": "K1; achieved = %d algorithmic warp-instr per DES event (SURVEY §8d.4 floor) x "
                                  "DES events / K1 time; peak = %d SMs x 4 issue/clk x %.0f MHz (MEASURED_PEAKS "
                                  "sm_max_mhz)" % (ALG_WARP_INSTR_PER_DES_EVENT, n_sm, f_mhz)},
