@@ -353,6 +353,7 @@ sdas_status plan(const sdas_pipeline* p, const sdas_grid* g, Plan& pl) {
     I.off_ftick = (uint32_t)o; o += 4ull * I.flight_cap;
     o = align_up(o, 16);
     I.off_fbody = (uint32_t)o; o += 8ull * I.flight_cap;
+    if (h.kv_role && I.role == h.kv_role) o += 4ull * I.flight_cap;    // hinted-transfer ready ticks (M23)
     o = align_up(o, 16);
     I.off_wait = (uint32_t)o; o += 4ull * I.wait_cap * (h.cls ? 2 : 1);
     o = align_up(o, 16);

@@ -73,8 +73,9 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
   const uint32_t kv_role = P.kv_role;
   const bool my_kv = kv_role != 0 && is_inst && my_role == kv_role;
   uint32_t* const my_iready = reinterpret_cast<uint32_t*>(my_inbox + 8u * my_inbox_cap);
-  const uint32_t my_hint_off =
-      my_kv ? P.kv_tau * P.kv_ctx - P.link[P.role[kv_role].in_link].net : 0u;   // ready = delivery + this
+  // per in-flight entry of a KV-role instance: the tick its hinted transfer completes (emission + tau*ctx,
+  // M23 HINT) -- kept beside the ring because pacing (M30) separates dispatch from emission
+  uint32_t* const my_fready = reinterpret_cast<uint32_t*>(my_fbody + 8u * my_flight_cap);
   uint8_t* const rHome = Wr + P.off_reqHome;
   uint8_t* const rCls = Wr + P.off_reqCls;                        // f2: class per request slot
   uint8_t* const rec_cls = reinterpret_cast<uint8_t*>(work) + P.off_rec_cls + gwarp * N;
@@ -280,6 +281,8 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
       if (lane == 0) {
         at<uint32_t>(Wr, D.off_ftick)[idx] = tick;
         at<unsigned long long>(Wr, D.off_fbody)[idx] = make_body(slot, flags, tokens, n_in);
+        if (kv_role && P.link[l].dst == kv_role)          // M23 HINT: the transfer starts at routing
+          at<uint32_t>(Wr, D.off_fbody + 8u * D.flight_cap)[idx] = t_lo + P.kv_tau * P.kv_ctx;
       }
       if (lane == (int)dest) {
         if (fn == 0) fhead = tick;
@@ -958,7 +961,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
             } else {
               const uint32_t at_idx = wrap_add(ih, in - (CLS ? in1 : 0u), my_inbox_cap);
               ib[at_idx] = body;
-              if (my_kv) my_iready[at_idx] = fhead + my_hint_off;   // emission + tau*ctx (M23 HINT)
+              if (my_kv) my_iready[at_idx] = my_fready[fh];        // emission + tau*ctx (M23 HINT)
             }
             ++in;
             fh = wrap_add(fh, 1u, my_flight_cap);
