@@ -96,7 +96,7 @@ class Candidate(C.Structure):
                 ("q_hi", C.c_uint32), ("select_role", C.c_int32), ("policy_slo", C.c_uint64),
                 ("kv_policy", C.c_uint32), ("guard_links", C.c_uint32), ("guard_pct", C.c_uint32),
                 ("prio", C.c_uint32), ("admit", C.c_uint32), ("admit_lo", C.c_uint32), ("admit_hi", C.c_uint32),
-                ("pacing_gap", C.c_uint32)]
+                ("pacing_gap", C.c_uint32), ("stale_jsq", C.c_uint32)]
 
 
 class Pipeline(C.Structure):
@@ -218,6 +218,7 @@ def _candidate(c, n_links):
     x.admit = 1 if c.get("admit") else 0
     x.admit_lo, x.admit_hi = c.get("admit_band", (400, 800))
     x.pacing_gap = 0xFFFFFFFF if c.get("pacing_gap") is None else int(c["pacing_gap"])
+    x.stale_jsq = 1 if c.get("stale_jsq") else 0
     return x
 
 

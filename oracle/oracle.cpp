@@ -241,6 +241,7 @@ struct Inst {
   // window accumulators (M15)
   uint64_t w_busy = 0, w_qint = 0, w_lint = 0;
   uint32_t w_maxq = 0;
+  uint32_t snap = 0;                 // M31: load polled at the last window close (state-store view)
   uint32_t Q() const { return (uint32_t)(inbox.size() + wait.size()); }
   uint32_t load() const {
     return inflight + (uint32_t)inbox.size() + (state == RECV ? 1u : 0u) + (uint32_t)wait.size() +
@@ -310,7 +311,7 @@ struct Replica {
     if (pol == ORC_FIXED) return f + R.route_fixed;
     if (pol == ORC_SELECT) return sel[role];
     std::vector<uint32_t> loads(n);
-    for (uint32_t i = 0; i < n; ++i) loads[i] = inst[f + i].load();
+    for (uint32_t i = 0; i < n; ++i) loads[i] = cand.stale_jsq ? inst[f + i].snap : inst[f + i].load();
     return f + jsq(loads.data(), n);
   }
 
@@ -686,6 +687,8 @@ struct Replica {
       if (cand.adaptive) control((int64_t)k + 1);
     }
     for (Inst& I : inst) { I.w_busy = I.w_qint = I.w_lint = 0; I.w_maxq = 0; }
+    if (!final_partial)               // M31: the controller's poll of every instance's load
+      for (Inst& I : inst) I.snap = I.load();
     w_n = w_good = w_half = 0;
   }
 

@@ -71,6 +71,7 @@ typedef struct {
   uint32_t admit;                 /* M28 (f2): admission gate on the source role's busy fraction */
   uint32_t admit_lo, admit_hi;    /*   reopen at <= lo, interactive-only at >= hi (permille) */
   uint32_t pacing_gap;            /* M30 (f4): 0xFFFFFFFF = each link's own gap, else this gap on every link */
+  uint32_t stale_jsq;             /* M31 (f4): JSQ ranks the loads polled at the last window close */
 } orc_candidate;
 
 typedef struct {

@@ -9,7 +9,7 @@ import pytest
 
 import oracle
 import workloads as W
-from gpu_parity import compare_records, compare_summaries, run_gpu
+from gpu_parity import compare_records, compare_summaries, full_check, run_gpu
 from paper_2601_03197_b200 import sdas
 
 pytestmark = pytest.mark.gpu
@@ -51,3 +51,13 @@ def test_config2_full_size_sampled():
     assert int(cnt[:, F["n_replicas"]].sum()) == R
     assert int(cnt[:, F["arrivals"]].sum()) == int(summ["arrivals"].astype(np.int64).sum())
     assert int(cnt[:, F["mode_switches"]].sum()) == int(summ["mode_switches"].astype(np.int64).sum())
+
+
+def test_max_requests_and_full_batches():
+    """N = 65535 requests per replica (SDAS_MAX_REQUESTS) with B = 32 (every lane a sequence), bit-exact."""
+    p = W.p2_x()
+    p["roles"][0]["max_num_seqs"] = 32
+    p["roles"][1]["max_num_seqs"] = 32
+    g = W.grid([W.static("token"), W.static("batch")], [W.poisson(1_300_000)], n_seeds=2, n_requests=65535)
+    gg, o = full_check(p, g, threads=4)
+    assert (gg["summary"]["completed"] == 65535).all()

@@ -91,3 +91,39 @@ def test_pacing_bounds_link_rate_and_conserves():
         assert ok.any()
         assert (paced["makespan"][ok] >= (paced["deliveries"][ok].astype(np.int64) - 1) * 20000).all()
         assert (paced["sum_e2e"][ok] >= free["sum_e2e"][ok]).all()
+
+
+# ------------------------------------------------------------------ M31 snapshot (stale) JSQ routing
+def _fanout2(route="jsq", window=1_000_000):
+    # dev -> tester x 2 (SPEC.md:469 route(): least_queue_depth on the latest Snapshot, ties -> lowest id)
+    dev = W.role("dev", c=W.cost(h=0), max_num_seqs=8, n_functions=2)
+    tester = W.role("tester", 2, W.cost(h=2000), max_num_seqs=4, out=(0, 1, 1), route=route, route_fixed=0)
+    return W.pipeline([dev, tester], [W.link(0, 1, net=500, chunk=8, mode="function")], window=window)
+
+
+def test_stale_jsq_without_a_poll_is_fixed_zero():
+    g = W.grid([dict(W.static("function"), stale_jsq=True)], [W.poisson(300_000, output=(32, 64))], n_seeds=3,
+               n_requests=200)
+    a = oracle.simulate(_fanout2(window=10 ** 12), g)["summary"]   # no window closes before the end
+    gf = W.grid([W.static("function")], g["arrivals"], n_seeds=3, n_requests=200)
+    b = oracle.simulate(_fanout2(route="fixed", window=10 ** 12), gf)["summary"]
+    for f in ("status", "completed", "sum_e2e", "sum_ff", "makespan", "deliveries", "decode_steps"):
+        assert (a[f] == b[f]).all(), f
+
+
+def test_stale_jsq_sends_each_window_to_one_instance():
+    Wn = 400_000
+    p = _fanout2(window=Wn)
+    g = W.grid([dict(W.static("function"), stale_jsq=True), W.static("function")],
+               [W.poisson(150_000, output=(32, 64))], n_requests=150)
+    dests = {}
+    for rid in (0, 1):
+        tr = oracle.simulate(p, g, trace_id=rid)["trace"]
+        per_w = {}
+        for r in tr:
+            if r["code"] == 6 and (int(r["c"]) >> 16) & 1:          # TR_EMIT of an opening message
+                per_w.setdefault(int(r["tick"]) // Wn, set()).add(int(r["a"]))
+        dests[rid] = per_w
+    assert all(len(v) == 1 for v in dests[0].values())                # stale: one instance per window
+    assert {d for v in dests[0].values() for d in v} == {1, 2}       # ... that changes between windows
+    assert any(len(v) == 2 for v in dests[1].values())                # live JSQ splits within a window
