@@ -173,6 +173,9 @@ typedef struct {
   uint32_t admit_lo_permille, admit_hi_permille; /* gate opens at <= lo, interactive-only at >= hi */
   uint32_t pacing_gap;        /* M30 (f4): 0xFFFFFFFF = every link's own pacing_gap knob; else this gap
                                  (0..2^18 ticks) on every link */
+  uint32_t stale_jsq;         /* M31 (f4): 1 = JSQ routing ranks the per-instance loads polled at the last
+                                 window close (the controller's state-store snapshot, SPEC.md:469 route()
+                                 on the latest Snapshot) instead of the live loads; 0 = live JSQ (M11) */
   uint64_t policy_slo_ticks;  /* SLO used by the controller's window p99 test */
 } sdas_candidate;
 

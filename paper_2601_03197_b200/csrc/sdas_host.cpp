@@ -203,6 +203,7 @@ sdas_status plan(const sdas_pipeline* p, const sdas_grid* g, Plan& pl) {
     if (cd.metric > SDAS_METRIC_LOAD || cd.lo_permille > 1000000 || cd.hi_permille > 1000000 || cd.dwell_windows > (1u << 30))
       return fail(SDAS_E_INVALID_FIELD, "cand[%u]: metric/lo/hi/dwell out of range", c);
     if (cd.prio > 1 || cd.admit > 1) return fail(SDAS_E_INVALID_FIELD, "cand[%u].prio/admit: 0 or 1", c);
+    if (cd.stale_jsq > 1) return fail(SDAS_E_INVALID_FIELD, "cand[%u].stale_jsq: 0 or 1", c);
     if (cd.admit && (cd.kind != SDAS_ADAPTIVE || cd.admit_lo_permille > cd.admit_hi_permille ||
                      cd.admit_hi_permille > 65535))
       return fail(SDAS_E_INVALID_FIELD, "cand[%u].admit: needs ADAPTIVE and admit_lo <= admit_hi <= 65535", c);
@@ -430,6 +431,7 @@ void pack_blob(const sdas_grid* g, const Plan& pl, std::vector<uint8_t>& blob) {
     d.admit_lo = (uint16_t)s.admit_lo_permille;
     d.admit_hi = (uint16_t)s.admit_hi_permille;
     d.pace = s.pacing_gap;
+    d.stale_jsq = s.stale_jsq ? 1u : 0u;
   }
   const uint64_t nIK = (uint64_t)g->n_rates * g->n_profiles;
   DArr* da = reinterpret_cast<DArr*>(blob.data() + pl.hp.off_arr);

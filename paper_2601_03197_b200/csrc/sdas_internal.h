@@ -38,7 +38,7 @@ struct DCand {          // one candidate, 80 B
   uint8_t band[4];
   uint32_t route_override, batch_roles, q_hi;
   int32_t select_role;
-  uint8_t kv_policy, guard_links, guard_pct, pad0;   // guard: M25 (f3)
+  uint8_t kv_policy, guard_links, guard_pct, stale_jsq;   // guard: M25 (f3); stale_jsq: M31 (f4)
   uint64_t policy_slo;
   uint32_t prio, admit;                              // f2: M27 priority service, M28 admission gate
   uint16_t admit_lo, admit_hi;

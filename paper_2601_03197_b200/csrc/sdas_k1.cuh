@@ -120,6 +120,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
     int32_t qlB = -(1 << 30);
     uint32_t acc_busy = 0, acc_maxq = 0, cnt_deliv = 0, cnt_recv = 0, cnt_decode = 0, n_large = 0, cnt_kv = 0;
     uint32_t H_next = 0;   // KV home (index within kv_role) of the next arriving request (M21)
+    uint32_t snap = 0;     // M31: this instance's load polled at the last window close (stale JSQ)
     // A DECODE "run" is runm consecutive steps of one unchanged batch of which all but the last are
     // silent (no emission point, no finish, no first feedback, no admission, empty inbox): they change
     // nothing any other part of the model observes, so they complete as one event at end_lo with the
@@ -238,7 +239,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
       if (pol == SDAS_ROUTE_SELECT) return __shfl_sync(FULL, sel_l, role);
       uint32_t key = 0xFFFFFFFFu;
       if (lane >= (int)R.first && lane < (int)(R.first + R.n)) {
-        const uint32_t load = fn + in + (st == RECV ? 1u : 0u) + wn + b;
+        const uint32_t load = cd.stale_jsq ? snap : fn + in + (st == RECV ? 1u : 0u) + wn + b;
         key = (load << 4) | (uint32_t)(lane - R.first);
       }
       key = __reduce_min_sync(FULL, key);
@@ -897,6 +898,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
         if (cd.adaptive) control((int32_t)wk + 1);
       }
       acc_busy = 0; acc_qint = 0; acc_lint = 0; acc_maxq = 0;
+      if (!final_partial) snap = fn + in + (st == RECV ? 1u : 0u) + wn + b;   // M31: the controller's poll
       __syncwarp();
       if (lane == 0) { H->w_n = 0; H->w_good = 0; H->w_half = 0; }
     };

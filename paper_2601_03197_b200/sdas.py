@@ -96,7 +96,7 @@ class Candidate(C.Structure):
                 ("q_hi", C.c_uint32), ("select_role", C.c_int32), ("kv_policy", C.c_uint32),
                 ("guard_links", C.c_uint32), ("guard_pct", C.c_uint32), ("prio", C.c_uint32), ("admit", C.c_uint32),
                 ("admit_lo_permille", C.c_uint32), ("admit_hi_permille", C.c_uint32), ("pacing_gap", C.c_uint32),
-                ("policy_slo_ticks", C.c_uint64)]
+                ("stale_jsq", C.c_uint32), ("policy_slo_ticks", C.c_uint64)]
 
 
 class Constraint(C.Structure):
@@ -234,6 +234,7 @@ def _candidate(c, n_links):
     x.admit = 1 if c.get("admit") else 0
     x.admit_lo_permille, x.admit_hi_permille = c.get("admit_band", (400, 800))
     x.pacing_gap = 0xFFFFFFFF if c.get("pacing_gap") is None else int(c["pacing_gap"])
+    x.stale_jsq = 1 if c.get("stale_jsq") else 0
     return x
 
 
@@ -253,7 +254,7 @@ def _candidate_dict(x, n_links):
             "kv": kvinv[x.kv_policy], "guard_links": [l for l in range(n_links) if (x.guard_links >> l) & 1],
             "guard_pct": x.guard_pct, "prio": bool(x.prio), "admit": bool(x.admit),
             "admit_band": (x.admit_lo_permille, x.admit_hi_permille),
-            "pacing_gap": None if x.pacing_gap == 0xFFFFFFFF else x.pacing_gap}
+            "pacing_gap": None if x.pacing_gap == 0xFFFFFFFF else x.pacing_gap, "stale_jsq": bool(x.stale_jsq)}
 
 
 def compile_intent(pipeline, objective=None, constraints=(), rules=None):

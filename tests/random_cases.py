@@ -4,7 +4,7 @@ Each case: a DAG of 1-4 roles (fan-out <= 2, one in-link per role, 1-2 instances
 FIXED routing), LLM roles and tools (det / exp service), random costs, capacities, chunks, modes and
 pacing gaps, Poisson / DET / MMPP-2 arrivals, and candidates mixing static modes, the three-band
 controller (busy / load), SLO batch control, route overrides, M25 guards, f2 priority / admission
-(with request classes) or f1 KV policies, and pacing overrides."""
+(with request classes) or f1 KV policies, pacing overrides and snapshot (stale) JSQ."""
 import numpy as np
 
 import workloads as W
@@ -15,6 +15,7 @@ MODES = ["batch", "function", "token"]
 
 def make_case(seed):
     r = np.random.default_rng(1000 + seed)
+    rs = np.random.default_rng(5000 + seed)
     n_roles = int(r.integers(1, 5))
     n_inst = [1] * n_roles
     for k in range(1, n_roles):
@@ -91,6 +92,8 @@ def make_case(seed):
             c = W.with_kv(c, str(r.choice(list(W.KV_POLICIES))))
         if nl and r.random() < 0.2:
             c = W.with_pacing(c, int(r.choice([0, 1000, 5000])))
+        if rs.random() < 0.3:                        # M31 (own stream: earlier draws are unchanged)
+            c = W.with_stale_jsq(c)
         cands.append(c)
     g = W.grid(cands, arrs, n_seeds=2, n_requests=int(r.choice([60, 150])),
                max_ticks=int(r.choice([0, 0, 0, 40_000_000])))

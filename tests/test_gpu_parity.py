@@ -306,3 +306,30 @@ def test_pacing_with_fanout_routing_and_classes():
     g["arrivals"] = [[W.with_classes(a, 300) for a in row] for row in g["arrivals"]]
     g["candidates"] = [W.with_prio(c, k % 2 == 0) for k, c in enumerate(g["candidates"][:6])]
     full_check(p, g)
+
+
+# ------------------------------------------------------------------ f4: snapshot (stale) JSQ routing (M31)
+def _fanout2(window=400_000):
+    dev = W.role("dev", c=W.cost(h=0), max_num_seqs=8, n_functions=2)
+    tester = W.role("tester", 2, W.cost(h=2000), max_num_seqs=4, out=(0, 1, 1), route="jsq")
+    return W.pipeline([dev, tester], [W.link(0, 1, net=500, chunk=8, mode="function")], window=window)
+
+
+def test_stale_jsq_trace_and_grid():
+    p = _fanout2()
+    g = W.grid([W.with_stale_jsq(W.static(m)) for m in ("function", "token", "batch")] + [W.static("function")],
+               [W.poisson(150_000, output=(32, 64)), W.poisson(90_000, output=(16, 64))], n_seeds=4,
+               n_requests=300)
+    full_check(p, g, series=False)
+    gg = run_gpu(p, g, trace_replica=0)
+    assert first_divergence(sorted_trace(gg["trace"]), sorted_trace(oracle.simulate(p, g, trace_id=0)["trace"])) is None
+
+
+def test_stale_jsq_config3_with_controller_and_stepwise():
+    # config-3 DAG (JSQ coder x 2, tester x 2) with stale JSQ on every other candidate
+    p, g = W.config3(n_seeds=2, n_requests=250)
+    g["candidates"] = [W.with_stale_jsq(c, k % 2 == 0) for k, c in enumerate(g["candidates"])]
+    full_check(p, g, objective="p99_e2e")
+    a = run_gpu(p, g)
+    b = run_gpu(p, g, stepwise=True)
+    assert a["summary"].tobytes() == b["summary"].tobytes()

@@ -376,6 +376,13 @@ def with_pacing(cand, gap):
     return c
 
 
+def with_stale_jsq(cand, stale=True):
+    """Candidate whose JSQ routing ranks the loads polled at the last window close (M31)."""
+    c = copy.deepcopy(cand)
+    c["stale_jsq"] = bool(stale)
+    return c
+
+
 def config_pace(n_seeds=8, n_requests=1000, gaps=(1597600, 726182, 469882),
                 pacing=(0, 2000, 8000, 20000)):
     """f4 workload: P2-X with token streaming / per-function pipelining, swept over the link pacing gap
