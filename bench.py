@@ -165,6 +165,7 @@ def main():
     ap.add_argument("--ref-sample", type=int, default=512)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--generic", action="store_true", help="A/B only: disable the LEAN K1 specialisation")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
@@ -192,14 +193,15 @@ def main():
         g["seed_offset"] = step * S_total                              # fresh synthetic input per step
         return g
 
-    gv0 = sdas.GridView(pipe, grid_for(0), rank=rank, world=world)
+    kflags = sdas.FLAG_GENERIC if args.generic else 0
+    gv0 = sdas.GridView(pipe, grid_for(0), flags=kflags, rank=rank, world=world)
     L = sdas.results_layout(P, gv0)
     res = sdas.Result(L, sdas.allocate(L, dev, 0))
     acc_local = torch.zeros(sdas.NCNT, dtype=torch.int64, device=dev)
     acc_global = torch.zeros(sdas.NCNT, dtype=torch.int64, device=dev)
 
     def one_step(step, timed, ev):
-        gv = sdas.GridView(pipe, grid_for(step), rank=rank, world=world)
+        gv = sdas.GridView(pipe, grid_for(step), flags=kflags, rank=rank, world=world)
         res.t["cell_cnt"].zero_()
         res.t["cell_hist"].zero_()
         flush.fill_(step & 0xFF)                                       # L2 flush before the step

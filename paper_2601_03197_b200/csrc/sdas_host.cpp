@@ -331,6 +331,12 @@ sdas_status plan(const sdas_pipeline* p, const sdas_grid* g, Plan& pl) {
   h.max_out = 1;
   for (uint32_t r = 0; r < h.n_roles; ++r) h.max_out = std::max(h.max_out, h.role[r].n_out);
   for (uint32_t r = 0; r < h.n_roles; ++r) h.role[r].batch_words = 1 + 2 * h.max_out;
+  // LEAN K1: one instance per role (routing, model selection and snapshot JSQ are
+  // identities), no fan-out, no KV modelling, no pacing, no request classes, no LOAD-metric integral
+  h.lean = (g->flags & SDAS_FLAG_GENERIC) == 0 && h.n_inst == h.n_roles && h.max_out == 1 && !h.kv_role &&
+           !h.need_pace && !h.need_lint && !h.cls && (h.flags & SDAS_FLAG_TRACE) == 0;
+  for (uint32_t cc = 0; cc < g->n_candidates; ++cc)
+    if (g->cand[cc].select_role >= 0) h.lean = 0;
 
   // --- shared-memory layout of one warp's replica
   uint64_t o = 256;  // WarpHdr
@@ -379,7 +385,7 @@ sdas_status plan(const sdas_pipeline* p, const sdas_grid* g, Plan& pl) {
     const uint64_t sb = h.off_warps + (uint64_t)wpb * h.smem_per_warp;
     if (sb > smem_cap) break;
     int bps = 0, nsm = 0;
-    if (query_occupancy(wpb, (uint32_t)sb, h.max_out, h.cls, &bps, &nsm) == 0 && bps > 0) {
+    if (query_occupancy(wpb, (uint32_t)sb, h.max_out, h.cls, h.lean, &bps, &nsm) == 0 && bps > 0) {
       have_dev = true;
       n_sm = nsm;
     } else {
@@ -477,6 +483,7 @@ sdas_status fill_layout(const Plan& pl, const sdas_grid* g, sdas_layout* L) {
   L->warps_per_block = pl.wpb;
   L->blocks_per_sm = pl.blocks_per_sm;
   L->resident_replicas = pl.total_warps;
+  L->k1_variant = h.lean;
   return SDAS_OK;
 }
 

@@ -64,7 +64,7 @@ struct alignas(16) DParams {
   uint32_t off_reqA, off_reqFF, off_reqJ, off_reqO, off_reqNit, off_reqOut, off_bitmap, off_scratch;
   uint32_t max_out, need_lint, kv_role, kv_ctx, kv_tau, off_reqHome;
   uint32_t cls, off_reqCls;   // f2: two request classes (class-1 rings follow the class-0 rings)
-  uint32_t need_pace, pad_pace;   // f4: some link or candidate paces (M30)
+  uint32_t need_pace, lean;   // f4: some link or candidate paces (M30); lean: K1 specialisation (§5.3)
   uint64_t off_rec_cls;       // f2: byte offset in `work` of the per-warp record-class arrays
   uint64_t kv_skew32;         // M21: home = instance 0 iff ATTR.w2 < kv_skew32 = floor(skew * 2^32 / 1000)
   uint64_t window, slo, max_ticks, master_seed;
@@ -94,7 +94,7 @@ int launch_group_argmin(const uint8_t* params_dev, const DParams& hp, const sdas
                         uint64_t slo, void* stream);
 int launch_finalize(const uint8_t* params_dev, const DParams& hp, const sdas_buffers* b, uint32_t objective,
                     uint64_t slo, uint64_t n_cells, uint64_t n_rows, void* stream);
-int query_occupancy(uint32_t warps_per_block, uint32_t smem_bytes, uint32_t maxout, uint32_t cls, int* blocks_per_sm,
+int query_occupancy(uint32_t warps_per_block, uint32_t smem_bytes, uint32_t maxout, uint32_t cls, uint32_t lean, int* blocks_per_sm,
                     int* n_sm);
 const char* cuda_error_string(int code);
 

@@ -35,7 +35,7 @@ OBJECTIVES = {"p99_e2e": 0, "p50_e2e": 1, "p99_ff": 2, "throughput": 3, "goodput
 INTENTS = {None: 0, "max_throughput": 1, "min_p90_latency": 2}
 CONSTRAINT_METRICS = {"e2e_p90": 0, "e2e_p99": 1}
 SCOPES = {"replica": 0, "cell": 1, "group": 2, "row": 3}
-FLAG_RECORDS, FLAG_SERIES, FLAG_TRACE, FLAG_STEPWISE = 1, 2, 4, 8
+FLAG_RECORDS, FLAG_SERIES, FLAG_TRACE, FLAG_STEPWISE, FLAG_GENERIC = 1, 2, 4, 8, 16
 NBINS, NCNT, NHIST = 464, 28, 3
 ROUTE_NONE = 255
 
@@ -131,7 +131,8 @@ class Layout(C.Structure):
         "cell_hist_bytes", "best_group_bytes", "best_row_bytes", "trace_bytes", "n_local_replicas",
         "n_local_groups", "n_groups", "n_cells", "n_rows", "n_replicas")] + [
         ("n_instances", C.c_uint32), ("smem_per_replica", C.c_uint32), ("warps_per_block", C.c_uint32),
-        ("blocks_per_sm", C.c_uint32), ("resident_replicas", C.c_uint64)]
+        ("blocks_per_sm", C.c_uint32), ("resident_replicas", C.c_uint64), ("k1_variant", C.c_uint32),
+        ("pad", C.c_uint32)]
 
 
 BUFFER_NAMES = ["params", "work", "summary", "records", "series", "cell_cnt", "cell_hist", "best_group",

@@ -333,3 +333,32 @@ def test_stale_jsq_config3_with_controller_and_stepwise():
     a = run_gpu(p, g)
     b = run_gpu(p, g, stepwise=True)
     assert a["summary"].tobytes() == b["summary"].tobytes()
+
+
+# ------------------------------------------------------------------ LEAN K1 specialisation
+@pytest.mark.parametrize("cfg", ["config1", "config2", "config5", "tools"])
+def test_lean_kernel_equals_generic(cfg):
+    if cfg == "config1":
+        p, g = W.config1(n_seeds=2, n_requests=400)
+    elif cfg == "config2":
+        p, g = W.config2(n_seeds=2, n_requests=300, series_stride=7, series_windows=64)
+    elif cfg == "config5":
+        p, g = W.config5(n_seeds=1, n_requests=200, n_rates=8, n_candidates=64)
+    else:
+        p = W.tandem(60000, 70000, 1000, svc="exp")
+        g = W.grid([W.static("batch"), W.static("token")], [W.poisson(100000, output=(0, 0))], n_seeds=5,
+                   n_requests=400)
+    series = "series_slots" in g and cfg == "config2"
+    a = run_gpu(p, g, series=series)
+    assert a["res"].layout.k1_variant == 1
+    b = run_gpu(p, g, series=series, generic=True)
+    assert b["res"].layout.k1_variant == 0
+    assert a["summary"].tobytes() == b["summary"].tobytes()
+    compare_records(a["records"], b["records"], a["summary"])   # slots past `completed` are never written
+    if series:
+        assert a["series"].tobytes() == b["series"].tobytes()
+    for x, y in zip(a["cells"], b["cells"]):
+        assert x.tobytes() == y.tobytes()
+    o = oracle.simulate(p, g, series=series)
+    compare_summaries(a["summary"], o["summary"])
+    compare_records(a["records"], o["records"], a["summary"])
