@@ -17,6 +17,8 @@
 // LEAN: every role has one instance, no fan-out / KV / pacing / classes / LOAD metric --
 // routing is the identity and that code is compiled out, shrinking the I-cache-bound hot loop.
 
+#define K1_UNLIKELY(x) (x)   // marks cold branches (__builtin_expect layout measured +2 % slower)
+
 #ifndef K1_LB_THREADS
 #define K1_LB_THREADS 256   // 2 x 8 warps per SM at <= 128 registers
 #define K1_LB_BLOCKS 2
@@ -262,7 +264,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
         trace(TR_EMIT, dest, rJ[slot], tokens | ((flags & 1u) << 16) | (((flags >> 1) & 1u) << 17) | (l << 20));
       const DInst& D = P.inst[dest];
       const uint32_t fn_d = __shfl_sync(FULL, fn, dest);
-      if (fn_d >= D.flight_cap) {
+      if (K1_UNLIKELY(fn_d >= D.flight_cap)) {
         if (TRACE) trace(TR_OVERFLOW, 1, dest, 0);
         ovf = true;
         return;
@@ -364,7 +366,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
       if (!(flags & F_CLOSES)) return;
       if (out > 0) {
         const uint32_t wn_i = __shfl_sync(FULL, wn, i);
-        if (wn_i >= I.wait_cap) {
+        if (K1_UNLIKELY(wn_i >= I.wait_cap)) {
           if (TRACE) trace(TR_OVERFLOW, 2, i, 0);
           ovf = true;
           return;
@@ -388,7 +390,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
         const uint32_t dest = route(P.link[l].dst, slot);
         if (lane == 0) rO[slot] += 1u;
         push_msg(l, dest, slot, 0u, F_OPENS | F_CLOSES | (kv_kind(l, dest, slot) << 2), 0u);
-        if (ovf) return;
+        if (K1_UNLIKELY(ovf)) return;
       }
       if (lane == 0 && role == fb_role && rFF[slot] == kUnsetFF) rFF[slot] = sat32(t - rA[slot]);
       if (P.inst[i].flags & 1u) { if (lane == (int)i) ++n_large; }
@@ -488,7 +490,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
               const uint32_t fn_d = __shfl_sync(FULL, fn, dk), fh_d = __shfl_sync(FULL, fh, dk);
               const DInst& D = P.inst[dk];
               const uint32_t cnt = __popc(grp);
-              if (fn_d + cnt > D.flight_cap) {
+              if (K1_UNLIKELY(fn_d + cnt > D.flight_cap)) {
                 if (TRACE) trace(TR_OVERFLOW, 1, dk, 0);
                 ovf = true;
                 return;
@@ -526,7 +528,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
                 fkv |= kv_kind(l, dk, sk) << 2;
               }
               push_msg(l, dk, sk, tk, fkv, nk);
-              if (ovf) return;
+              if (K1_UNLIKELY(ovf)) return;
             }
           }
           if (eq) {
@@ -774,7 +776,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
           ++in;
           if (coalesce) cut_run();
         }
-        if (__ballot_sync(FULL, bad)) {
+        if (K1_UNLIKELY(__ballot_sync(FULL, bad))) {
           if (TRACE) trace(TR_OVERFLOW, 0, dest, 0);
           ovf = true;
         }
@@ -917,7 +919,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
       const uint32_t d0 = min(nb_lo - t_lo, arr_near ? A_lo - t_lo : 0xFFFFFFFFu);
       d = lane == 0 ? min(d, d0) : d;
       d = __reduce_min_sync(FULL, d);
-      if (max_ticks && t + d > max_ticks) { status = SDAS_REPLICA_TRUNCATED; break; }
+      if (K1_UNLIKELY(max_ticks && t + d > max_ticks)) { status = SDAS_REPLICA_TRUNCATED; break; }
       {  // integrate the piecewise-constant state over [t, t + d) (M15)
         const uint32_t Q = in + wn;
         acc_busy += st != IDLE ? d : 0u;
@@ -928,14 +930,15 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
       int_nsys += (unsigned long long)nsys * d;
       t += d;
       t_lo += d;
-      if (t_lo == nb_lo) {  // phase 0 WINDOW
+      if (K1_UNLIKELY(t_lo == nb_lo)) {  // phase 0 WINDOW
         close_window(false);
         nb_lo += W32;
         ++wk;
         if (!arr_near && jn < N) arr_near = A_next - t < 0x80000000ull;
       }
       // phase 1 COMPLETE (instance order)
-      const bool done_here = is_inst && st != IDLE && end_lo == t_lo;
+      // (lanes >= n_inst stay IDLE with empty rings: no is_inst test needed in the phase votes)
+      const bool done_here = st != IDLE && end_lo == t_lo;
       uint32_t cm = __ballot_sync(FULL, done_here);
       if (cm) {
         const uint32_t rm = __ballot_sync(FULL, done_here && st == RECV);
@@ -944,13 +947,15 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
           cm &= cm - 1;
           if ((rm >> i) & 1u) complete_recv((uint32_t)i);
           else complete_decode((uint32_t)i);
-          if (ovf) break;
+          if (K1_UNLIKELY(ovf)) break;
         } while (cm);
-        if (ovf) break;
+        if (K1_UNLIKELY(ovf)) break;
       }
       // phase 2 DELIVER (per destination instance, FIFO; lane = instance)
-      const bool dv = is_inst && fn > 0 && fhead == t_lo;
+      const bool dv = fn > 0 && fhead == t_lo;
+      bool cut = false;                    // a DELIVER or ARRIVE may have cut a DECODE run
       if (__ballot_sync(FULL, dv)) {
+        cut = true;
         bool lovf = false;
         if (dv) {
           if (coalesce) cut_run();
@@ -958,7 +963,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
           const unsigned long long* fb = reinterpret_cast<const unsigned long long*>(my_fbody);
           unsigned long long* ib = reinterpret_cast<unsigned long long*>(my_inbox);
           for (;;) {
-            if (in >= my_inbox_cap) { lovf = true; break; }
+            if (K1_UNLIKELY(in >= my_inbox_cap)) { lovf = true; break; }
             const unsigned long long body = fb[fh];
             if (CLS && prio && rCls[body & 0xFFFFu]) {        // M27: class-1 ring
               ib[my_inbox_cap + wrap_add(ih1, in1, my_inbox_cap)] = body;
@@ -978,7 +983,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
             if (fhead != t_lo) break;
           }
         }
-        if (__ballot_sync(FULL, lovf)) {
+        if (K1_UNLIKELY(__ballot_sync(FULL, lovf))) {
           if (TRACE) trace(TR_OVERFLOW, 0, 0, 0);
           ovf = true;
           break;
@@ -986,14 +991,15 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
         __syncwarp();
       }
       // phase 3 ARRIVE (increasing j)
-      if (arr_near && A_lo == t_lo) {
+      if (K1_UNLIKELY(arr_near && A_lo == t_lo)) {
+        cut = true;
         do {
           arrive();
         } while (!ovf && jn < N && arr_near && A_lo == t_lo);
-        if (ovf) break;
+        if (K1_UNLIKELY(ovf)) break;
       }
       // runs cut exactly at this tick: apply their silent steps (they precede START, as in M12)
-      if (coalesce) {
+      if (coalesce && cut) {
         uint32_t fm = __ballot_sync(FULL, flushm != 0u);
         while (fm) {
           const int i = __ffs(fm) - 1;
@@ -1015,7 +1021,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
       }
       // phase 4 START (idle instances with work, increasing index)
       __syncwarp();                        // wait-ring / request-table writes of this tick are visible
-      const bool can = is_inst && st == IDLE && (in | wn | b) != 0u;
+      const bool can = st == IDLE && (in | wn | b) != 0u;
       uint32_t sm = __ballot_sync(FULL, can);
       if (sm) {
         const uint32_t recvm = __ballot_sync(FULL, can && in != 0u);

@@ -22,7 +22,7 @@ d = {k: v[h.index(k)] for k in keys if k in h}
 d["units"] = {k: u[h.index(k)] for k in keys if k in h}
 m = re.search(r"replicas (\d+) des_events (\d+) msg_events (\d+)", open(log).read())
 R, des = int(m.group(1)), int(m.group(2))
-d["workload"] = "tools/profile_k1.py --seeds 16: config-2 grid, %d replicas x 1000 requests, %d DES events (1 launch)" % (R, des)
+d["workload"] = "tools/profile_k1.py: config-2 grid, %d replicas x 1000 requests, %d DES events (1 launch)" % (R, des)
 d["warp_instr_per_des_event"] = float(d["smsp__inst_executed.sum"]) / des
 scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 dram = sum(float(d[k]) * scale[d["units"][k]] for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
