@@ -1,9 +1,10 @@
-"""Full-size parity in the launch configuration bench.py times (BASELINE.json configs 1 and 2).
+"""Full-size parity in the launch configuration bench.py times (BASELINE.json configs 1-5).
 
 Config 1 (384 replicas x 10,000 requests) is compared in full: every summary, record, cell and both
 argmin tables.  Config 2 (1,048,576 replicas x 1000 requests, in-loop controller) runs entirely on
 the GPU exactly as bench.py runs it (flags 0, one sdas_control_sweep + sdas_finalize); the oracle
-recomputes a deterministic sample of replicas one by one and every summary field must match."""
+recomputes a deterministic sample of replicas one by one and every summary field must match.  Configs
+3-5 run at full size (3) or as 1M-replica slices of their full grids (4: 16.7M, 5: 64M), sampled the same way."""
 import numpy as np
 import pytest
 
@@ -61,3 +62,30 @@ def test_max_requests_and_full_batches():
     g = W.grid([W.static("token"), W.static("batch")], [W.poisson(1_300_000)], n_seeds=2, n_requests=65535)
     gg, o = full_check(p, g, threads=4)
     assert (gg["summary"]["completed"] == 65535).all()
+
+
+@pytest.mark.parametrize("cfg", ["config3", "config4", "config5"])
+def test_full_size_grid_sampled(cfg):
+    """Configs 3-5 at their full BASELINE sizes (replica coordinates of the full grid): config 3 whole
+    (1,048,576 replicas); configs 4 (16.7M) and 5 (64M) as a contiguous 1M-replica slice of groups taken
+    from the middle of the grid.  One sdas_control_sweep as bench.py launches it (flags 0); the oracle
+    recomputes a deterministic sample of the slice's replicas one by one."""
+    import torch
+    p, g = {"config3": W.config3, "config4": W.config4, "config5": W.config5}[cfg]()
+    C = len(g["candidates"])
+    G = W.grid_size(g) // C
+    n_groups = min(G, (1 << 20) // C)
+    g0 = ((G - n_groups) // 2 // n_groups) * n_groups
+    objective = "large_under_slo" if cfg == "config4" else "p99_e2e"
+    slo = 6_000_000 if cfg == "config4" else 0
+    P = sdas.Pipeline(p)
+    gv = sdas.GridView(p, g, group_range=(g0, g0 + n_groups))
+    res = sdas.control_sweep(P, gv, objective=objective, objective_slo=slo)
+    torch.cuda.synchronize()
+    summ = res.summary()
+    assert len(summ) == n_groups * C == 1 << 20
+    local = np.asarray(W.sample_ids(len(summ), 256), dtype=np.int64)
+    ids = (local + g0 * C).astype(np.uint64)
+    o = oracle.simulate(p, g, ids=ids, records=False, hists=False)
+    compare_summaries(summ[local], o["summary"], where="%s slice sample" % cfg)
+    assert int(summ["arrivals"].astype(np.int64).sum()) > 0
