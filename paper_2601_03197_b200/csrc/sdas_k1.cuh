@@ -392,6 +392,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
         push_msg(l, dest, slot, 0u, F_OPENS | F_CLOSES | (kv_kind(l, dest, slot) << 2), 0u);
         if (K1_UNLIKELY(ovf)) return;
       }
+      __syncwarp();                        // lane 0's ring writes precede the destinations' DELIVER reads
       if (lane == 0 && role == fb_role && rFF[slot] == kUnsetFF) rFF[slot] = sat32(t - rA[slot]);
       if (P.inst[i].flags & 1u) { if (lane == (int)i) ++n_large; }
       item_done(slot);
@@ -530,6 +531,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
               push_msg(l, dk, sk, tk, fkv, nk);
               if (K1_UNLIKELY(ovf)) return;
             }
+            __syncwarp();                  // lane 0's ring writes precede the destinations' DELIVER reads
           }
           if (eq) {
             if (q == 0) wC = (wC & 0x00FFFFFFu) | (sticky << 24);
@@ -538,8 +540,8 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
         }
       }
       if (role == fb_role) {  // first output token at a feedback-role instance (M13)
-        // (two items of one request may both reach done == 1 in this step: both store the same value)
-        if (act && done == 1u && rFF[slot] == kUnsetFF) rFF[slot] = sat32(t - rA[slot]);
+        // (two items of one request may both reach done == 1 in this step: the CAS lets the first set it)
+        if (act && done == 1u) atomicCAS(&rFF[slot], kUnsetFF, sat32(t - rA[slot]));
         __syncwarp();
       }
       const uint32_t fin = __ballot_sync(FULL, act && done == out);

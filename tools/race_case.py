@@ -12,6 +12,8 @@ cases = {
                                          series_windows=16)),
     "config3": lambda: W.config3(n_seeds=1, n_requests=60),
     "kv": lambda: W.config_kv(n_seeds=1, n_requests=80),
+    "prio": lambda: W.config_prio(n_seeds=1, n_requests=80, gaps=(726182,)),
+    "pace": lambda: W.config_pace(n_seeds=1, n_requests=80, gaps=(726182,)),
 }
 for name in (sys.argv[1:] or list(cases)):
     p, g = cases[name]()
@@ -19,4 +21,4 @@ for name in (sys.argv[1:] or list(cases)):
     flags = sdas.FLAG_RECORDS | (sdas.FLAG_SERIES if g["series_stride"] else 0)
     r = sdas.simulate(P, sdas.GridView(p, g, flags=flags))
     torch.cuda.synchronize()
-    print(name, "ok", int(r.summary()["completed"].sum()))
+    print(name, "ok", int(r.summary()["completed"].sum()), "k1_variant", r.layout.k1_variant)
