@@ -165,7 +165,8 @@ def main():
     ap.add_argument("--ref-sample", type=int, default=512)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--generic", action="store_true", help="A/B only: disable the LEAN K1 specialisation")
+    ap.add_argument("--generic", action="store_true", help="A/B only: disable the K1 specialisations")
+    ap.add_argument("--mid", action="store_true", help="A/B only: at most the level-1 K1 specialisation")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
@@ -193,7 +194,7 @@ def main():
         g["seed_offset"] = step * S_total                              # fresh synthetic input per step
         return g
 
-    kflags = sdas.FLAG_GENERIC if args.generic else 0
+    kflags = (sdas.FLAG_GENERIC if args.generic else 0) | (sdas.FLAG_MID if args.mid else 0)
     gv0 = sdas.GridView(pipe, grid_for(0), flags=kflags, rank=rank, world=world)
     L = sdas.results_layout(P, gv0)
     res = sdas.Result(L, sdas.allocate(L, dev, 0))

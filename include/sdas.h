@@ -66,8 +66,9 @@ enum { SDAS_SCOPE_REPLICA = 0, SDAS_SCOPE_CELL = 1, SDAS_SCOPE_GROUP = 2, SDAS_S
 #define SDAS_FLAG_TRACE 4u   /* write the event trace of grid.trace_replica (debug) */
 #define SDAS_FLAG_STEPWISE 8u /* simulate every DECODE step as its own event (no silent-run coalescing,
                                  DESIGN.md §5); results are identical either way -- A/B and debugging */
-#define SDAS_FLAG_GENERIC 16u /* never launch the specialised K1 for single-instance pipelines (DESIGN.md
-                                 §5.3); results are identical either way -- A/B and parity tests */
+#define SDAS_FLAG_GENERIC 16u /* never launch a specialised K1; results are identical
+                                 either way -- A/B and parity tests */
+#define SDAS_FLAG_MID 32u     /* at most the level-1 specialisation (A/B and parity tests) */
 
 /* implementation limits (DESIGN.md §"Limits") */
 #define SDAS_MAX_ROLES 8
@@ -231,7 +232,8 @@ typedef struct {
   uint64_t n_local_replicas, n_local_groups, n_groups, n_cells, n_rows, n_replicas;
   uint32_t n_instances, smem_per_replica, warps_per_block, blocks_per_sm;
   uint64_t resident_replicas;
-  uint32_t k1_variant;       /* 1 = the LEAN K1 specialisation runs this grid, 0 = generic */
+  uint32_t k1_variant;       /* K1 specialisation level running this grid: 0 generic,
+                                1 no KV / pacing / selection / classes / LOAD metric, 2 LEAN (+ single instances) */
   uint32_t pad;
 } sdas_layout;
 

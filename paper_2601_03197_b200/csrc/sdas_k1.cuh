@@ -14,8 +14,9 @@
 // CLS (f2, M26-M29): two request classes -- per-class inbox / wait rings (class-1 ring right after the
 // class-0 ring; used only under priority service, so FIFO across classes holds otherwise), the
 // admission gate, per-class metrics.  Pipelines without interactive requests never pay for it.
-// LEAN: every role has one instance, no fan-out / KV / pacing / classes / LOAD metric --
-// routing is the identity and that code is compiled out, shrinking the I-cache-bound hot loop.
+// LV: 0 generic; 1 = no KV / pacing / model selection / LOAD metric (compiled out);
+// 2 (LEAN) = level 1 + one instance per role and no fan-out: routing is the identity.  Shrinks the
+// I-cache-bound hot loop.
 
 #define K1_UNLIKELY(x) (x)   // marks cold branches (__builtin_expect layout measured +2 % slower)
 
@@ -23,7 +24,7 @@
 #define K1_LB_THREADS 256   // 2 x 8 warps per SM at <= 128 registers
 #define K1_LB_BLOCKS 2
 #endif
-template <bool TRACE, int MAXOUT, bool CLS, bool LEAN>
+template <bool TRACE, int MAXOUT, bool CLS, int LV>
 __global__ void __launch_bounds__(K1_LB_THREADS, K1_LB_BLOCKS)
 k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* __restrict__ summary,
             unsigned long long* __restrict__ records_out, uint8_t* __restrict__ series,
@@ -54,9 +55,10 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
   const uint32_t R_cap = P.request_cap, n_links = P.n_links;
   const uint32_t W32 = (uint32_t)P.window;
   const unsigned long long max_ticks = P.max_ticks;
-  const bool need_lint = !LEAN && P.need_lint != 0;
+  constexpr bool LEAN = LV >= 2;
+  const bool need_lint = LV == 0 && P.need_lint != 0;
   const bool coalesce = (P.flags & SDAS_FLAG_STEPWISE) == 0;   // silent DECODE runs
-  const bool need_pace = !LEAN && P.need_pace != 0;                     // f4 M30: some link is paced
+  const bool need_pace = LV == 0 && P.need_pace != 0;                     // f4 M30: some link is paced
   const uint32_t key0 = (uint32_t)P.master_seed, key1 = (uint32_t)(P.master_seed >> 32);
   const unsigned long long gwarp = (unsigned long long)blockIdx.x * (blockDim.x >> 5) + wib;
   unsigned long long* const rec_scratch =
@@ -74,7 +76,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
   uint8_t* const my_fbody = Wr + MI.off_fbody;
   const bool my_large = (MI.flags & 1u) != 0;
   // f1 (M21-M24): KV-role instances keep, per inbox entry, the tick a hinted transfer completes
-  const uint32_t kv_role = LEAN ? 0u : P.kv_role;
+  const uint32_t kv_role = LV ? 0u : P.kv_role;
   const bool my_kv = kv_role != 0 && is_inst && my_role == kv_role;
   uint32_t* const my_iready = reinterpret_cast<uint32_t*>(my_inbox + 8u * my_inbox_cap);
   // per in-flight entry of a KV-role instance: the tick its hinted transfer completes (emission + tau*ctx,
@@ -866,7 +868,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
           if (TRACE) trace(TR_CONTROL, 3, 0, want ? 1u : 0u);
         }
       }
-      if (!LEAN && cd.select_role >= 0) {  // (iii) model selection
+      if (LV == 0 && cd.select_role >= 0) {  // (iii) model selection
         const DRole& Rs = P.role[cd.select_role];
         const uint32_t cs = __shfl_sync(FULL, sel_l, cd.select_role);
         const unsigned long long b1000 = (unsigned long long)__shfl_sync(FULL, acc_busy, cs) * 1000ull;

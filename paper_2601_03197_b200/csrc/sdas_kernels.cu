@@ -301,20 +301,21 @@ __global__ void k5_row_argmin(const uint8_t* __restrict__ blob, const long long*
 // ------------------------------------------------------------------------------ launchers
 typedef void (*K1Fn)(const uint8_t*, Work*, uint8_t*, unsigned long long*, uint8_t*, long long*, int*, uint8_t*);
 
-static K1Fn k1_pick(bool trace, uint32_t maxout, bool cls, bool lean) {
-  if (lean && !trace && !cls && maxout == 1) return k1_simulate<false, 1, false, true>;
+static K1Fn k1_pick(bool trace, uint32_t maxout, bool cls, uint32_t lv) {
+  if (!trace && !cls && lv == 2 && maxout == 1) return k1_simulate<false, 1, false, 2>;
+  if (!trace && !cls && lv >= 1) return maxout > 1 ? k1_simulate<false, 2, false, 1> : k1_simulate<false, 1, false, 1>;
   if (cls) {
-    if (maxout > 1) return trace ? k1_simulate<true, 2, true, false> : k1_simulate<false, 2, true, false>;
-    return trace ? k1_simulate<true, 1, true, false> : k1_simulate<false, 1, true, false>;
+    if (maxout > 1) return trace ? k1_simulate<true, 2, true, 0> : k1_simulate<false, 2, true, 0>;
+    return trace ? k1_simulate<true, 1, true, 0> : k1_simulate<false, 1, true, 0>;
   }
-  if (maxout > 1) return trace ? k1_simulate<true, 2, false, false> : k1_simulate<false, 2, false, false>;
-  return trace ? k1_simulate<true, 1, false, false> : k1_simulate<false, 1, false, false>;
+  if (maxout > 1) return trace ? k1_simulate<true, 2, false, 0> : k1_simulate<false, 2, false, 0>;
+  return trace ? k1_simulate<true, 1, false, 0> : k1_simulate<false, 1, false, 0>;
 }
 
 int launch_simulate(const uint8_t* params_dev, const DParams& hp, const sdas_buffers* bf, uint32_t blocks,
                     uint32_t warps_per_block, uint32_t smem_bytes, void* stream, const uint64_t* log2_table) {
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  const K1Fn fn = k1_pick((hp.flags & SDAS_FLAG_TRACE) != 0, hp.max_out, hp.cls != 0, hp.lean != 0);
+  const K1Fn fn = k1_pick((hp.flags & SDAS_FLAG_TRACE) != 0, hp.max_out, hp.cls != 0, hp.lean);
   cudaError_t e = cudaMemcpyToSymbolAsync(c_log2, log2_table, sizeof(uint64_t) * 257, 0, cudaMemcpyHostToDevice, s);
   if (e != cudaSuccess) return (int)e;
   e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes);
@@ -376,7 +377,7 @@ int query_occupancy(uint32_t warps_per_block, uint32_t smem_bytes, uint32_t maxo
   if (e != cudaSuccess) return (int)e;
   e = cudaDeviceGetAttribute(n_sm, cudaDevAttrMultiProcessorCount, dev);
   if (e != cudaSuccess) return (int)e;
-  const K1Fn fn = k1_pick(false, maxout, cls != 0, lean != 0);
+  const K1Fn fn = k1_pick(false, maxout, cls != 0, lean);
   e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes);
   if (e != cudaSuccess) return (int)e;
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, fn, (int)warps_per_block * 32, smem_bytes);

@@ -35,7 +35,7 @@ OBJECTIVES = {"p99_e2e": 0, "p50_e2e": 1, "p99_ff": 2, "throughput": 3, "goodput
 INTENTS = {None: 0, "max_throughput": 1, "min_p90_latency": 2}
 CONSTRAINT_METRICS = {"e2e_p90": 0, "e2e_p99": 1}
 SCOPES = {"replica": 0, "cell": 1, "group": 2, "row": 3}
-FLAG_RECORDS, FLAG_SERIES, FLAG_TRACE, FLAG_STEPWISE, FLAG_GENERIC = 1, 2, 4, 8, 16
+FLAG_RECORDS, FLAG_SERIES, FLAG_TRACE, FLAG_STEPWISE, FLAG_GENERIC, FLAG_MID = 1, 2, 4, 8, 16, 32
 NBINS, NCNT, NHIST = 464, 28, 3
 ROUTE_NONE = 255
 

@@ -14,9 +14,10 @@ BINS = ["bin_p50_e2e", "bin_p99_e2e"]
 
 
 def run_gpu(pipe, grid, records=True, series=False, trace_replica=None, objective=None, objective_slo=0,
-            rank=0, world=1, group_range=None, stepwise=False, generic=False):
+            rank=0, world=1, group_range=None, stepwise=False, generic=False, mid=False):
     flags = (sdas.FLAG_RECORDS if records else 0) | (sdas.FLAG_SERIES if series else 0)
     flags |= (sdas.FLAG_STEPWISE if stepwise else 0) | (sdas.FLAG_GENERIC if generic else 0)
+    flags |= sdas.FLAG_MID if mid else 0
     P = sdas.Pipeline(pipe)
     gv = sdas.GridView(pipe, grid, flags=flags, rank=rank, world=world, group_range=group_range,
                        trace_replica=trace_replica, trace_cap=1 << 18)

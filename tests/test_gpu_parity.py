@@ -335,7 +335,16 @@ def test_stale_jsq_config3_with_controller_and_stepwise():
     assert a["summary"].tobytes() == b["summary"].tobytes()
 
 
-# ------------------------------------------------------------------ LEAN K1 specialisation
+# ------------------------------------------------------------------ K1 specialisation levels
+def _same_results(a, b, series):
+    assert a["summary"].tobytes() == b["summary"].tobytes()
+    compare_records(a["records"], b["records"], a["summary"])   # slots past `completed` are never written
+    if series:
+        assert a["series"].tobytes() == b["series"].tobytes()
+    for x, y in zip(a["cells"], b["cells"]):
+        assert x.tobytes() == y.tobytes()
+
+
 @pytest.mark.parametrize("cfg", ["config1", "config2", "config5", "tools"])
 def test_lean_kernel_equals_generic(cfg):
     if cfg == "config1":
@@ -348,17 +357,33 @@ def test_lean_kernel_equals_generic(cfg):
         p = W.tandem(60000, 70000, 1000, svc="exp")
         g = W.grid([W.static("batch"), W.static("token")], [W.poisson(100000, output=(0, 0))], n_seeds=5,
                    n_requests=400)
-    series = "series_slots" in g and cfg == "config2"
+    series = cfg == "config2"
     a = run_gpu(p, g, series=series)
-    assert a["res"].layout.k1_variant == 1
+    assert a["res"].layout.k1_variant == 2
     b = run_gpu(p, g, series=series, generic=True)
     assert b["res"].layout.k1_variant == 0
-    assert a["summary"].tobytes() == b["summary"].tobytes()
-    compare_records(a["records"], b["records"], a["summary"])   # slots past `completed` are never written
-    if series:
-        assert a["series"].tobytes() == b["series"].tobytes()
-    for x, y in zip(a["cells"], b["cells"]):
-        assert x.tobytes() == y.tobytes()
+    m = run_gpu(p, g, series=series, mid=True)
+    assert m["res"].layout.k1_variant == 1
+    _same_results(a, b, series)
+    _same_results(m, b, series)
     o = oracle.simulate(p, g, series=series)
+    compare_summaries(a["summary"], o["summary"])
+    compare_records(a["records"], o["records"], a["summary"])
+
+
+@pytest.mark.parametrize("cfg", ["config3", "fanout_stale"])
+def test_mid_kernel_equals_generic(cfg):
+    # routed pipelines without KV / pacing / selection / classes run the level-1 kernel
+    if cfg == "config3":
+        p, g = W.config3(n_seeds=2, n_requests=250)
+    else:
+        p, g = W.config3(n_seeds=2, n_requests=200)
+        g["candidates"] = [W.with_stale_jsq(c, k % 3 == 0) for k, c in enumerate(g["candidates"])]
+    a = run_gpu(p, g)
+    assert a["res"].layout.k1_variant == 1
+    b = run_gpu(p, g, generic=True)
+    assert b["res"].layout.k1_variant == 0
+    _same_results(a, b, False)
+    o = oracle.simulate(p, g)
     compare_summaries(a["summary"], o["summary"])
     compare_records(a["records"], o["records"], a["summary"])
