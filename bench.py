@@ -115,7 +115,13 @@ def cpu_baseline(args, target_s=15.0):
     msg = int(s["arrivals"].astype(np.int64).sum() + s["deliveries"].astype(np.int64).sum())
     des = msg + int(s["recv_steps"].astype(np.int64).sum() + s["decode_steps"].astype(np.int64).sum() +
                     s["window_closes"].astype(np.int64).sum())
+    ids1 = W.sample_ids(R, 48)                                 # single-thread rate
+    t1 = time.perf_counter()
+    s1 = oracle.simulate(pipe, grid, ids=ids1, threads=1, records=False, hists=False)["summary"]
+    dt1 = time.perf_counter() - t1
+    msg1 = int(s1["arrivals"].astype(np.int64).sum() + s1["deliveries"].astype(np.int64).sum())
     return {"value": msg / dt, "unit": UNIT, "cores": threads, "kind": "oracle",
+            "single_thread": {"value": msg1 / dt1, "unit": UNIT, "sample": "%d replicas" % len(ids1)},
             "sample": "%d of %d config-2 replicas (every floor(R/n)-th id + last), N=%d requests, %.1f s" % (
                 len(ids), R, args.requests, dt),
             "replicas_per_s": len(ids) / dt, "des_events_per_s": des / dt, "seconds": dt}
