@@ -9,7 +9,15 @@
 //   items (PAPER.md:17 the three strategies), M11 routing,
 //   M12 canonical tick order, M13 completion, M14 capacity, M15 windows
 //   (PAPER.md:231-238 metrics plane), M16 control (PAPER.md:18, 196-220,
-//   279-280), M17/M18 bins and nearest-rank percentiles, M19 summary, M20 argmin.
+//   279-280), M17/M18 bins and nearest-rank percentiles, M19 summary, M20 argmin;
+//   f1 M21-M24 KV home / routing / transfer penalty, f3 M25
+//   constraint guard, f2 M26-M29 request classes, priority service,
+//   admission gate, per-class metrics, f4 M30 pacing and M31
+//   snapshot JSQ.
+//
+// Parity unpinned: the full model at scale (batching + RECV-first + modes +
+// control) has no closed form; it is pinned compositionally by the hand traces, queueing
+// closed forms, conservation laws and brute-force checks under tests/test_oracle_*.py.
 //
 // Deliberately naive: std::priority_queue of events, std::deque queues,
 // std::vector<Item> batches, std::sort for percentiles.  No code is shared with
