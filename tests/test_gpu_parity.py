@@ -345,10 +345,15 @@ def _same_results(a, b, series):
         assert x.tobytes() == y.tobytes()
 
 
-@pytest.mark.parametrize("cfg", ["config1", "config2", "config5", "tools"])
+@pytest.mark.parametrize("cfg", ["config1", "config2", "config5", "tools", "truncated_mmpp"])
 def test_lean_kernel_equals_generic(cfg):
     if cfg == "config1":
         p, g = W.config1(n_seeds=2, n_requests=400)
+    elif cfg == "truncated_mmpp":               # MMPP-2 arrivals and max_ticks truncation on LEAN
+        p = W.p2_x()
+        g = W.grid([W.static("token"), W.static("batch"), W.adaptive(["function"], dwell=2)],
+                   [W.mmpp2(900_000, 200_000, 20_000_000, 8_000_000)], n_seeds=6, n_requests=300,
+                   max_ticks=160_000_000)
     elif cfg == "config2":
         p, g = W.config2(n_seeds=2, n_requests=300, series_stride=7, series_windows=64)
     elif cfg == "config5":
