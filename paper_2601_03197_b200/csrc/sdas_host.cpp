@@ -387,9 +387,10 @@ sdas_status plan(const sdas_pipeline* p, const sdas_grid* g, Plan& pl) {
     const uint64_t sb = h.off_warps + (uint64_t)wpb * h.smem_per_warp;
     if (sb > smem_cap) break;
     int bps = 0, nsm = 0;
-    if (query_occupancy(wpb, (uint32_t)sb, h.max_out, h.cls, h.lean, &bps, &nsm) == 0 && bps > 0) {
+    if (query_occupancy(wpb, (uint32_t)sb, h.max_out, h.cls, h.lean, &bps, &nsm) == 0) {
       have_dev = true;
       n_sm = nsm;
+      if (bps <= 0) continue;                 // block exceeds the instantiation's launch bound
     } else {
       bps = (int)std::min<uint64_t>(32, (228 * 1024) / (sb + 1024));
       bps = std::min(bps, (int)(64 / wpb));

@@ -22,13 +22,19 @@
 
 #ifndef K1_LB_THREADS
 #define K1_LB_THREADS 256   // 2 x 8 warps per SM at <= 128 registers
-#define K1_LB_BLOCKS 2
+#define K1_LB_MAXREG 128
+#endif
+#ifndef K1_LEAN_THREADS     // the LEAN level's own bounds (A/B: -DK1_LEAN_THREADS=192 -DK1_LEAN_MAXREG=112)
+#define K1_LEAN_THREADS K1_LB_THREADS
+#define K1_LEAN_MAXREG K1_LB_MAXREG
 #endif
 template <bool TRACE, int MAXOUT, bool CLS, int LV>
-__global__ void __launch_bounds__(K1_LB_THREADS, K1_LB_BLOCKS)
+__global__ void __launch_bounds__(LV == 2 ? K1_LEAN_THREADS : K1_LB_THREADS)
+__maxnreg__(LV == 2 ? K1_LEAN_MAXREG : K1_LB_MAXREG)
 k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* __restrict__ summary,
             unsigned long long* __restrict__ records_out, uint8_t* __restrict__ series,
-            long long* __restrict__ cell_cnt, int* __restrict__ cell_hist, uint8_t* __restrict__ trace_buf) {
+            long long* __restrict__ cell_cnt, int* __restrict__ cell_hist, uint8_t* __restrict__ trace_buf,
+            const __grid_constant__ DParams Pk) {   // scalars from parameter space (uniform registers)
   extern __shared__ __align__(16) uint8_t smem[];
   {
     const uint4* src = reinterpret_cast<const uint4*>(blob);
@@ -39,32 +45,32 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
   const DParams& P = *reinterpret_cast<const DParams*>(smem);
   const int lane = threadIdx.x & 31;
   const uint32_t wib = threadIdx.x >> 5;
-  uint8_t* const Wr = smem + P.off_warps + wib * P.smem_per_warp;
+  uint8_t* const Wr = smem + Pk.off_warps + wib * Pk.smem_per_warp;
   WarpHdr* const H = reinterpret_cast<WarpHdr*>(Wr);
-  unsigned long long* const rA = at<unsigned long long>(Wr, P.off_reqA);
-  uint32_t* const rFF = at<uint32_t>(Wr, P.off_reqFF);
-  uint32_t* const rJ = at<uint32_t>(Wr, P.off_reqJ);
-  uint32_t* const rO = at<uint32_t>(Wr, P.off_reqO);
-  uint16_t* const rNit = at<uint16_t>(Wr, P.off_reqNit);
-  uint16_t* const rOut = at<uint16_t>(Wr, P.off_reqOut);
-  uint32_t* const bitmap = at<uint32_t>(Wr, P.off_bitmap);
-  uint32_t* const scratch = at<uint32_t>(Wr, P.off_scratch);
+  unsigned long long* const rA = at<unsigned long long>(Wr, Pk.off_reqA);
+  uint32_t* const rFF = at<uint32_t>(Wr, Pk.off_reqFF);
+  uint32_t* const rJ = at<uint32_t>(Wr, Pk.off_reqJ);
+  uint32_t* const rO = at<uint32_t>(Wr, Pk.off_reqO);
+  uint16_t* const rNit = at<uint16_t>(Wr, Pk.off_reqNit);
+  uint16_t* const rOut = at<uint16_t>(Wr, Pk.off_reqOut);
+  uint32_t* const bitmap = at<uint32_t>(Wr, Pk.off_bitmap);
+  uint32_t* const scratch = at<uint32_t>(Wr, Pk.off_scratch);
 
   // hoisted constants
-  const uint32_t N = P.n_requests, C = P.C, n_inst = P.n_inst, fb_role = P.feedback_role;
-  const uint32_t R_cap = P.request_cap, n_links = P.n_links;
-  const uint32_t W32 = (uint32_t)P.window;
-  const unsigned long long max_ticks = P.max_ticks;
+  const uint32_t N = Pk.n_requests, C = P.C, n_inst = Pk.n_inst, fb_role = Pk.feedback_role;
+  const uint32_t R_cap = Pk.request_cap, n_links = Pk.n_links;
+  const uint32_t W32 = (uint32_t)Pk.window;
+  const unsigned long long max_ticks = Pk.max_ticks;
   constexpr bool LEAN = LV >= 2;
-  const bool need_lint = LV == 0 && P.need_lint != 0;
-  const bool coalesce = (P.flags & SDAS_FLAG_STEPWISE) == 0;   // silent DECODE runs
-  const bool need_pace = LV == 0 && P.need_pace != 0;                     // f4 M30: some link is paced
-  const uint32_t key0 = (uint32_t)P.master_seed, key1 = (uint32_t)(P.master_seed >> 32);
+  const bool need_lint = LV == 0 && Pk.need_lint != 0;
+  const bool coalesce = (Pk.flags & SDAS_FLAG_STEPWISE) == 0;   // silent DECODE runs
+  const bool need_pace = LV == 0 && Pk.need_pace != 0;                     // f4 M30: some link is paced
+  const uint32_t key0 = (uint32_t)Pk.master_seed, key1 = (uint32_t)(Pk.master_seed >> 32);
   const unsigned long long gwarp = (unsigned long long)blockIdx.x * (blockDim.x >> 5) + wib;
   unsigned long long* const rec_scratch =
       reinterpret_cast<unsigned long long*>(reinterpret_cast<uint8_t*>(work) + sizeof(Work)) + gwarp * N;
-  const DCand* const cands = reinterpret_cast<const DCand*>(blob + P.off_cand);
-  const DArr* const arrs = reinterpret_cast<const DArr*>(blob + P.off_arr);
+  const DCand* const cands = reinterpret_cast<const DCand*>(blob + Pk.off_cand);
+  const DArr* const arrs = reinterpret_cast<const DArr*>(blob + Pk.off_arr);
 
   // lane-resident constants of instance `lane`
   const bool is_inst = lane < (int)n_inst;
@@ -76,31 +82,31 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
   uint8_t* const my_fbody = Wr + MI.off_fbody;
   const bool my_large = (MI.flags & 1u) != 0;
   // f1 (M21-M24): KV-role instances keep, per inbox entry, the tick a hinted transfer completes
-  const uint32_t kv_role = LV ? 0u : P.kv_role;
+  const uint32_t kv_role = LV ? 0u : Pk.kv_role;
   const bool my_kv = kv_role != 0 && is_inst && my_role == kv_role;
   uint32_t* const my_iready = reinterpret_cast<uint32_t*>(my_inbox + 8u * my_inbox_cap);
   // per in-flight entry of a KV-role instance: the tick its hinted transfer completes (emission + tau*ctx,
   // M23 HINT) -- kept beside the ring because pacing (M30) separates dispatch from emission
   uint32_t* const my_fready = reinterpret_cast<uint32_t*>(my_fbody + 8u * my_flight_cap);
-  uint8_t* const rHome = Wr + P.off_reqHome;
-  uint8_t* const rCls = Wr + P.off_reqCls;                        // f2: class per request slot
-  uint8_t* const rec_cls = reinterpret_cast<uint8_t*>(work) + P.off_rec_cls + gwarp * N;
+  uint8_t* const rHome = Wr + Pk.off_reqHome;
+  uint8_t* const rCls = Wr + Pk.off_reqCls;                        // f2: class per request slot
+  uint8_t* const rec_cls = reinterpret_cast<uint8_t*>(work) + Pk.off_rec_cls + gwarp * N;
 
   for (;;) {
     unsigned long long x = 0;
     if (lane == 0) x = atomicAdd(&work->next_replica, 1ull);
     x = __shfl_sync(FULL, x, 0);
-    if (x >= P.n_local_replicas) break;
+    if (x >= Pk.n_local_replicas) break;
 
     // ---------------------------------------------------------------- replica coordinates (M1)
     const uint32_t c = (uint32_t)(x % C);
-    const unsigned long long g = P.first_group + (x / C) * P.world;
-    const uint32_t s_coord = (uint32_t)(g % P.S) + P.seed_offset;
+    const unsigned long long g = Pk.first_group + (x / C) * Pk.world;
+    const uint32_t s_coord = (uint32_t)(g % P.S) + Pk.seed_offset;
     const DCand& cd = cands[c];
     const DArr& ad = arrs[(g / P.S) % (P.I * (unsigned long long)P.K)];
-    const bool trace_on = TRACE && g * C + c == P.trace_replica;
+    const bool trace_on = TRACE && g * C + c == Pk.trace_replica;
     unsigned long long* const rec =
-        (P.flags & SDAS_FLAG_RECORDS) ? records_out + x * (unsigned long long)N : rec_scratch;
+        (Pk.flags & SDAS_FLAG_RECORDS) ? records_out + x * (unsigned long long)N : rec_scratch;
 
     // ---------------------------------------------------------------- init
     // Warp discipline (independent thread scheduling): warp-uniform scalars live in registers or are
@@ -111,9 +117,9 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
       modes |= (uint32_t)(cd.mode[l] == 255 ? P.link[l].mode : cd.mode[l]) << (2 * l);
     int32_t qlm = -(1 << 30), q_last_sel = -(1 << 30);   // lane l: last change of link l's mode
     uint32_t rr_l = 0;                                    // lane r: round-robin counter of role r
-    uint32_t sel_l = lane < (int)P.n_roles ? P.role[lane].large_inst : 0u;  // lane r: SELECT target
+    uint32_t sel_l = lane < (int)Pk.n_roles ? P.role[lane].large_inst : 0u;  // lane r: SELECT target
     if (lane == 0) *H = WarpHdr{};
-    for (uint32_t w = lane; w < P.bitmap_words; w += 32) {
+    for (uint32_t w = lane; w < Pk.bitmap_words; w += 32) {
       const uint32_t rem = R_cap - w * 32;
       bitmap[w] = rem >= 32 ? 0xFFFFFFFFu : ((1u << rem) - 1u);
     }
@@ -152,7 +158,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
     auto trace = [&](uint32_t code, uint32_t a, uint32_t bb, uint32_t cc) {
       if (TRACE && trace_on && lane == 0) {
         const unsigned long long k = atomicAdd(reinterpret_cast<unsigned long long*>(trace_buf), 1ull);
-        if (k < P.trace_cap) {
+        if (k < Pk.trace_cap) {
           TraceRec* r = reinterpret_cast<TraceRec*>(trace_buf + 8) + k;
           r->tick = t; r->code = code; r->a = a; r->b = bb; r->c = cc;
         }
@@ -161,7 +167,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
     auto trace_at = [&](unsigned long long tick, uint32_t code, uint32_t a, uint32_t bb, uint32_t cc) {
       if (TRACE && trace_on && lane == 0) {
         const unsigned long long k = atomicAdd(reinterpret_cast<unsigned long long*>(trace_buf), 1ull);
-        if (k < P.trace_cap) {
+        if (k < Pk.trace_cap) {
           TraceRec* r = reinterpret_cast<TraceRec*>(trace_buf + 8) + k;
           r->tick = tick; r->code = code; r->a = a; r->b = bb; r->c = cc;
         }
@@ -179,7 +185,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
     auto trace_lane = [&](uint32_t code, uint32_t a, uint32_t bb, uint32_t cc) {
       if (TRACE && trace_on) {
         const unsigned long long k = atomicAdd(reinterpret_cast<unsigned long long*>(trace_buf), 1ull);
-        if (k < P.trace_cap) {
+        if (k < Pk.trace_cap) {
           TraceRec* r = reinterpret_cast<TraceRec*>(trace_buf + 8) + k;
           r->tick = t; r->code = code; r->a = a; r->b = bb; r->c = cc;
         }
@@ -216,7 +222,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
       const uint4 w = philox4(j, s_coord, 2u << 16, 0u, key0, key1);
       P_next = uni(ad.p_lo, ad.p_hi, w.x);
       O_next = uni(ad.o_lo, ad.o_hi, w.y);
-      if (kv_role) H_next = (unsigned long long)w.z < P.kv_skew32 ? 0u : uni(0u, P.role[kv_role].n - 1u, w.w);
+      if (kv_role) H_next = (unsigned long long)w.z < Pk.kv_skew32 ? 0u : uni(0u, P.role[kv_role].n - 1u, w.w);
       if (CLS) C_next = (unsigned long long)philox(j, s_coord, 2u << 16, 1u, key0, key1).x < ad.ithr ? 1u : 0u;
       arr_near = A_next - t < 0x80000000ull;
       A_lo = (uint32_t)A_next;
@@ -289,7 +295,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
         at<uint32_t>(Wr, D.off_ftick)[idx] = tick;
         at<unsigned long long>(Wr, D.off_fbody)[idx] = make_body(slot, flags, tokens, n_in);
         if (kv_role && P.link[l].dst == kv_role)          // M23 HINT: the transfer starts at routing
-          at<uint32_t>(Wr, D.off_fbody + 8u * D.flight_cap)[idx] = t_lo + P.kv_tau * P.kv_ctx;
+          at<uint32_t>(Wr, D.off_fbody + 8u * D.flight_cap)[idx] = t_lo + Pk.kv_tau * Pk.kv_ctx;
       }
       if (lane == (int)dest) {
         if (fn == 0) fhead = tick;
@@ -313,14 +319,14 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
           if (ci) {
             ++h.completed_int;
             h.sum_e2e_int += e2e;
-            h.good_int += e2e <= P.slo ? 1u : 0u;
+            h.good_int += e2e <= Pk.slo ? 1u : 0u;
           }
         }
         ++h.completed;
         h.sum_e2e += e2e;
         h.sum_ff += f32;
         h.max_e2e = max(h.max_e2e, e32);
-        h.good += e2e <= P.slo ? 1u : 0u;
+        h.good += e2e <= Pk.slo ? 1u : 0u;
         ++h.w_n;
         const unsigned long long ps = cd.policy_slo;
         h.w_good += e2e <= ps ? 1u : 0u;
@@ -604,8 +610,8 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
           const uint32_t kvk = (flags >> 2) & 7u;
           if (kvk) {  // M23: KV penalty of an opening RECV away from the request's KV home
             uint32_t pen;
-            if (kvk == SDAS_KV_RECOMPUTE) pen = MI.beta * P.kv_ctx;
-            else if (kvk == SDAS_KV_POSTHOC) pen = P.kv_tau * P.kv_ctx;
+            if (kvk == SDAS_KV_RECOMPUTE) pen = MI.beta * Pk.kv_ctx;
+            else if (kvk == SDAS_KV_POSTHOC) pen = Pk.kv_tau * Pk.kv_ctx;
             else pen = (uint32_t)max(0, (int32_t)(my_iready[ih] - t_lo));
             cost += pen;
             ++cnt_kv;
@@ -747,7 +753,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
         if (lane == 0) ++H->admitted;
         ++nsys;
         __syncwarp();
-        const uint32_t wv = lane < (int)P.bitmap_words ? bitmap[lane] : 0u;   // lowest free slot
+        const uint32_t wv = lane < (int)Pk.bitmap_words ? bitmap[lane] : 0u;   // lowest free slot
         const uint32_t wm = __ballot_sync(FULL, wv != 0);
         const int wi = __ffs(wm) - 1;
         const uint32_t word = __shfl_sync(FULL, wv, wi);
@@ -809,8 +815,8 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
               warp_sum64(mine ? (cd.metric_load ? acc_lint : (unsigned long long)acc_busy) : 0ull);
           const unsigned long long lhs = u * 1000ull;
           uint32_t band = 1;
-          if (lhs >= (unsigned long long)cd.hi * P.window * Rd.n) band = 2;
-          else if (lhs <= (unsigned long long)cd.lo * P.window * Rd.n) band = 0;
+          if (lhs >= (unsigned long long)cd.hi * Pk.window * Rd.n) band = 2;
+          else if (lhs <= (unsigned long long)cd.lo * Pk.window * Rd.n) band = 0;
           want = cd.band[band];
         } else if (w_n >= 1) {
           want = cd.mode[l] == 255 ? P.link[l].mode : cd.mode[l];   // reset to the initial mode
@@ -836,7 +842,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
         bool changed = false;
         if (is_inst && ((cd.batch_roles >> my_role) & 1u)) {
           uint32_t nbB = Bk;
-          if (viol) nbB = acc_qint > (unsigned long long)cd.q_hi * P.window ? min(32u, 2u * Bk) : max(1u, Bk / 2u);
+          if (viol) nbB = acc_qint > (unsigned long long)cd.q_hi * Pk.window ? min(32u, 2u * Bk) : max(1u, Bk / 2u);
           else if (calm) nbB = MI.B_default;
           if (nbB != Bk && q - qlB >= (int32_t)cd.dwell) {
             Bk = nbB;
@@ -859,8 +865,8 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
         const bool mine = lane >= (int)R0.first && lane < (int)(R0.first + R0.n);
         const unsigned long long u1000 = warp_sum64(mine ? (unsigned long long)acc_busy : 0ull) * 1000ull;
         bool want = gate;
-        if (u1000 >= (unsigned long long)cd.admit_hi * P.window * R0.n) want = true;
-        else if (u1000 <= (unsigned long long)cd.admit_lo * P.window * R0.n) want = false;
+        if (u1000 >= (unsigned long long)cd.admit_hi * Pk.window * R0.n) want = true;
+        else if (u1000 <= (unsigned long long)cd.admit_lo * Pk.window * R0.n) want = false;
         if (want != gate && q - q_last_gate >= (int32_t)cd.dwell) {
           gate = want;
           q_last_gate = q;
@@ -873,8 +879,8 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
         const uint32_t cs = __shfl_sync(FULL, sel_l, cd.select_role);
         const unsigned long long b1000 = (unsigned long long)__shfl_sync(FULL, acc_busy, cs) * 1000ull;
         uint32_t ns = cs;
-        if (b1000 >= (unsigned long long)cd.hi * P.window || viol) ns = Rs.small_inst;
-        else if (b1000 <= (unsigned long long)cd.lo * P.window && !viol) ns = Rs.large_inst;
+        if (b1000 >= (unsigned long long)cd.hi * Pk.window || viol) ns = Rs.small_inst;
+        else if (b1000 <= (unsigned long long)cd.lo * Pk.window && !viol) ns = Rs.large_inst;
         if (ns != cs && q - q_last_sel >= (int32_t)cd.dwell) {
           if (lane == cd.select_role) sel_l = ns;
           q_last_sel = q;
@@ -885,13 +891,13 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
     };
     auto close_window = [&](bool final_partial) {
       SeriesRec* ser = nullptr;
-      if ((P.flags & SDAS_FLAG_SERIES) && P.series_stride) {
-        const unsigned long long rid = (P.first_group + (x / C) * P.world) * C + c;
-        if (rid % P.series_stride == 0 && rid / P.series_stride < P.series_slots)
+      if ((Pk.flags & SDAS_FLAG_SERIES) && Pk.series_stride) {
+        const unsigned long long rid = (Pk.first_group + (x / C) * Pk.world) * C + c;
+        if (rid % Pk.series_stride == 0 && rid / Pk.series_stride < Pk.series_slots)
           ser = reinterpret_cast<SeriesRec*>(series) +
-                (rid / P.series_stride) * (unsigned long long)P.series_windows * n_inst;
+                (rid / Pk.series_stride) * (unsigned long long)Pk.series_windows * n_inst;
       }
-      if (ser && wk < P.series_windows && is_inst) {
+      if (ser && wk < Pk.series_windows && is_inst) {
         const int32_t il = P.role[my_role].in_link;
         SeriesRec r;
         r.qint = acc_qint;

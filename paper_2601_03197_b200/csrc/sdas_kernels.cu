@@ -299,7 +299,8 @@ __global__ void k5_row_argmin(const uint8_t* __restrict__ blob, const long long*
 }
 
 // ------------------------------------------------------------------------------ launchers
-typedef void (*K1Fn)(const uint8_t*, Work*, uint8_t*, unsigned long long*, uint8_t*, long long*, int*, uint8_t*);
+typedef void (*K1Fn)(const uint8_t*, Work*, uint8_t*, unsigned long long*, uint8_t*, long long*, int*, uint8_t*,
+                     DParams);
 
 static K1Fn k1_pick(bool trace, uint32_t maxout, bool cls, uint32_t lv) {
   if (!trace && !cls && lv == 2 && maxout == 1) return k1_simulate<false, 1, false, 2>;
@@ -335,7 +336,7 @@ int launch_simulate(const uint8_t* params_dev, const DParams& hp, const sdas_buf
       params_dev, reinterpret_cast<Work*>(bf->work), reinterpret_cast<uint8_t*>(bf->summary),
       reinterpret_cast<unsigned long long*>(bf->records), reinterpret_cast<uint8_t*>(bf->series),
       reinterpret_cast<long long*>(bf->cell_cnt), reinterpret_cast<int*>(bf->cell_hist),
-      reinterpret_cast<uint8_t*>(bf->trace));
+      reinterpret_cast<uint8_t*>(bf->trace), hp);
   return (int)cudaGetLastError();
 }
 
@@ -372,6 +373,18 @@ int launch_finalize(const uint8_t* params_dev, const DParams& hp, const sdas_buf
 
 int query_occupancy(uint32_t warps_per_block, uint32_t smem_bytes, uint32_t maxout, uint32_t cls, uint32_t lean,
                     int* blocks_per_sm, int* n_sm) {
+  {  // a block larger than the instantiation's launch bound cannot launch
+    cudaFuncAttributes fa;
+    const cudaError_t ea = cudaFuncGetAttributes(&fa, k1_pick(false, maxout, cls != 0, lean));
+    if (ea != cudaSuccess) return (int)ea;
+    if ((int)(warps_per_block * 32) > fa.maxThreadsPerBlock) {
+      *blocks_per_sm = 0;
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(n_sm, cudaDevAttrMultiProcessorCount, dev);
+      return 0;
+    }
+  }
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return (int)e;
