@@ -75,7 +75,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
   // lane-resident constants of instance `lane`
   const bool is_inst = lane < (int)n_inst;
   const DInst& MI = P.inst[is_inst ? lane : 0];
-  const uint32_t my_role = MI.role;
+  const uint32_t my_role = LEAN ? (uint32_t)lane : MI.role;
   const uint32_t my_inbox_cap = MI.inbox_cap, my_flight_cap = MI.flight_cap, my_wait_cap = MI.wait_cap;
   uint8_t* const my_inbox = Wr + MI.off_inbox;
   uint8_t* const my_ftick = Wr + MI.off_ftick;
@@ -348,7 +348,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
     // ---------------------------------------------------------------- phase COMPLETE: RECV (M8, M10)
     auto complete_recv = [&](uint32_t i) {
       const DInst& I = P.inst[i];
-      const uint32_t role = I.role;
+      const uint32_t role = LEAN ? i : I.role;      // LEAN: instance i is role i's only instance
       const DRole& R = P.role[role];
       const unsigned long long body = __shfl_sync(FULL, cur, i);
       const uint32_t slot = (uint32_t)(body & 0xFFFFu), flags = (uint32_t)(body >> 16) & 0xFFu;
@@ -409,7 +409,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
     // ---------------------------------------------------------------- phase COMPLETE: DECODE (M7, M9, M13)
     auto complete_decode = [&](uint32_t i) {
       const DInst& I = P.inst[i];
-      const uint32_t role = I.role;
+      const uint32_t role = LEAN ? i : I.role;      // LEAN: instance i is role i's only instance
       const DRole& R = P.role[role];
       const uint32_t bi = __shfl_sync(FULL, b, i);
       const uint32_t mi = __shfl_sync(FULL, runm, i);          // steps in this run (all but the last silent)
@@ -478,7 +478,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
           if (single || openers == 0) {
             // every message of this link goes to a known instance: place them in parallel
             // (per-destination order = batch order; M9/M11 sticky continuations)
-            const uint32_t dest_single = Rd.first;
+            const uint32_t dest_single = LEAN ? P.link[l].dst : Rd.first;   // LEAN: role r = instance r
             uint32_t dest = (single || (flags & 1u)) ? dest_single : sticky;
             if (single && eq && (flags & 1u)) sticky = dest_single;
             // M30 pacing: the link's messages of this step leave in batch order, gp apart
@@ -634,7 +634,8 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
     };
     auto start_decode = [&](uint32_t i) {  // FIFO admission (modes bound here, M9) + DECODE step / run
       const DInst& I = P.inst[i];
-      const DRole& R = P.role[I.role];
+      const uint32_t role = LEAN ? i : I.role;
+      const DRole& R = P.role[role];
       const uint32_t bi = __shfl_sync(FULL, b, i), Bi = __shfl_sync(FULL, Bk, i);
       const uint32_t wn_i = __shfl_sync(FULL, wn, i);
       const uint32_t nadm = Bi > bi ? min(Bi - bi, wn_i) : 0u;
@@ -691,7 +692,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
           uint32_t lim = wA >> 16;                                      // out
           if (n_out > 0) lim = min(lim, wB >> 16);
           if (MAXOUT > 1 && n_out > 1) lim = min(lim, wD & 0xFFFFu);
-          sk = (I.role == fb_role && done == 0u) ? 1u : lim - done;
+          sk = (role == fb_role && done == 0u) ? 1u : lim - done;
         }
         m = __reduce_min_sync(FULL, sk);
         if (m > 1) {
@@ -809,14 +810,16 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
         if (grd && gviol) {
           want = SDAS_BATCH;
         } else if (ctl) {
-          const DRole& Rd = P.role[P.link[l].dst];
-          const bool mine = lane >= (int)Rd.first && lane < (int)(Rd.first + Rd.n);
+          const uint32_t dst = P.link[l].dst;
+          const DRole& Rd = P.role[dst];
+          const uint32_t rd_first = LEAN ? dst : Rd.first, rd_n = LEAN ? 1u : Rd.n;
+          const bool mine = lane >= (int)rd_first && lane < (int)(rd_first + rd_n);
           const unsigned long long u =
               warp_sum64(mine ? (cd.metric_load ? acc_lint : (unsigned long long)acc_busy) : 0ull);
           const unsigned long long lhs = u * 1000ull;
           uint32_t band = 1;
-          if (lhs >= (unsigned long long)cd.hi * Pk.window * Rd.n) band = 2;
-          else if (lhs <= (unsigned long long)cd.lo * Pk.window * Rd.n) band = 0;
+          if (lhs >= (unsigned long long)cd.hi * Pk.window * rd_n) band = 2;
+          else if (lhs <= (unsigned long long)cd.lo * Pk.window * rd_n) band = 0;
           want = cd.band[band];
         } else if (w_n >= 1) {
           want = cd.mode[l] == 255 ? P.link[l].mode : cd.mode[l];   // reset to the initial mode
