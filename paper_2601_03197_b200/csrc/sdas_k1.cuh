@@ -57,13 +57,13 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
   uint32_t* const scratch = at<uint32_t>(Wr, Pk.off_scratch);
 
   // hoisted constants
-  const uint32_t N = Pk.n_requests, C = P.C, n_inst = Pk.n_inst, fb_role = Pk.feedback_role;
+  const uint32_t N = Pk.n_requests, C = Pk.C, n_inst = Pk.n_inst, fb_role = Pk.feedback_role;
   const uint32_t R_cap = Pk.request_cap, n_links = Pk.n_links;
   const uint32_t W32 = (uint32_t)Pk.window;
-  const unsigned long long max_ticks = Pk.max_ticks;
   constexpr bool LEAN = LV >= 2;
+  const unsigned long long max_ticks = LEAN ? 0ull : Pk.max_ticks;   // LEAN grids never truncate
   const bool need_lint = LV == 0 && Pk.need_lint != 0;
-  const bool coalesce = (Pk.flags & SDAS_FLAG_STEPWISE) == 0;   // silent DECODE runs
+  const bool coalesce = LEAN || (Pk.flags & SDAS_FLAG_STEPWISE) == 0;   // silent DECODE runs
   const bool need_pace = LV == 0 && Pk.need_pace != 0;                     // f4 M30: some link is paced
   const uint32_t key0 = (uint32_t)Pk.master_seed, key1 = (uint32_t)(Pk.master_seed >> 32);
   const unsigned long long gwarp = (unsigned long long)blockIdx.x * (blockDim.x >> 5) + wib;
@@ -101,9 +101,9 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
     // ---------------------------------------------------------------- replica coordinates (M1)
     const uint32_t c = (uint32_t)(x % C);
     const unsigned long long g = Pk.first_group + (x / C) * Pk.world;
-    const uint32_t s_coord = (uint32_t)(g % P.S) + Pk.seed_offset;
+    const uint32_t s_coord = (uint32_t)(g % Pk.S) + Pk.seed_offset;
     const DCand& cd = cands[c];
-    const DArr& ad = arrs[(g / P.S) % (P.I * (unsigned long long)P.K)];
+    const DArr& ad = arrs[(g / Pk.S) % (Pk.I * (unsigned long long)Pk.K)];
     const bool trace_on = TRACE && g * C + c == Pk.trace_replica;
     unsigned long long* const rec =
         (Pk.flags & SDAS_FLAG_RECORDS) ? records_out + x * (unsigned long long)N : rec_scratch;
@@ -112,7 +112,8 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
     // Warp discipline (independent thread scheduling): warp-uniform scalars live in registers or are
     // lane-distributed; shared scalars are read-modify-written by lane 0 only and broadcast by shfl;
     // __syncwarp() orders cross-lane shared-memory traffic at phase boundaries.
-    uint32_t modes = 0;                                   // current mode per link, 2 bits each (M16 state)
+    // current mode per link, 2 bits each (M16 state); bit 31 caches cd.adaptive (a register, not a global load)
+    uint32_t modes = cd.adaptive ? 0x80000000u : 0u;
     for (uint32_t l = 0; l < n_links; ++l)
       modes |= (uint32_t)(cd.mode[l] == 255 ? P.link[l].mode : cd.mode[l]) << (2 * l);
     int32_t qlm = -(1 << 30), q_last_sel = -(1 << 30);   // lane l: last change of link l's mode
@@ -700,7 +701,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
           // controller could change B while items wait; never step past max_ticks
           if ((unsigned long long)m * cost32 >= (1ull << 30)) m = max(1u, (1u << 30) / cost32);
           const uint32_t span = m * cost32;
-          if (cd.adaptive && wn_i > nadm) {
+          if ((modes >> 31) && wn_i > nadm) {
             const uint32_t nbd = nb_lo - t_lo;
             if (span > nbd) m = (nbd + cost32 - 1u) / cost32;
           }
@@ -1050,7 +1051,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
     // ---------------------------------------------------------------- finalize (M18, M19)
     uint8_t* const sum_out = summary + x * SDAS_SUMMARY_BYTES;
     const unsigned long long rid = g * C + c;
-    const unsigned long long cell = ((g / P.S) % (P.I * (unsigned long long)P.K)) * C + c;
+    const unsigned long long cell = ((g / Pk.S) % (Pk.I * (unsigned long long)Pk.K)) * C + c;
     uint32_t* const stg = scratch + SDAS_NHIST * SDAS_NBINS + 256;   // 40 summary words, then counters
     unsigned long long* const cst = reinterpret_cast<unsigned long long*>(stg + 40);
     __syncwarp();
