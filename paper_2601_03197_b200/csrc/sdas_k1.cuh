@@ -112,8 +112,9 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
     // Warp discipline (independent thread scheduling): warp-uniform scalars live in registers or are
     // lane-distributed; shared scalars are read-modify-written by lane 0 only and broadcast by shfl;
     // __syncwarp() orders cross-lane shared-memory traffic at phase boundaries.
-    // current mode per link, 2 bits each (M16 state); bit 31 caches cd.adaptive (a register, not a global load)
-    uint32_t modes = cd.adaptive ? 0x80000000u : 0u;
+    // current mode per link, 2 bits each (M16 state, bits 0-13); bits 28-30 cache the feedback role and
+    // bit 31 cd.adaptive, so the hot paths test them from a register instead of a parameter / global load
+    uint32_t modes = (cd.adaptive ? 0x80000000u : 0u) | (fb_role << 28);
     for (uint32_t l = 0; l < n_links; ++l)
       modes |= (uint32_t)(cd.mode[l] == 255 ? P.link[l].mode : cd.mode[l]) << (2 * l);
     int32_t qlm = -(1 << 30), q_last_sel = -(1 << 30);   // lane l: last change of link l's mode
@@ -151,7 +152,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
     // uniform replica state
     unsigned long long t = 0, A_next = 0, int_nsys = 0;
     uint32_t t_lo = 0, nb_lo = W32, A_lo = 0, jn = 0, P_next = 0, O_next = 0, nsys = 0, wk = 0;
-    bool arr_near = false, ovf = false;
+    bool arr_near = false, ovf = false, arr_more = N > 0;
     uint32_t status = SDAS_REPLICA_OK;
     uint32_t mm_k = 0;
     unsigned long long mm_end = 0;
@@ -402,7 +403,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
         if (K1_UNLIKELY(ovf)) return;
       }
       __syncwarp();                        // lane 0's ring writes precede the destinations' DELIVER reads
-      if (lane == 0 && role == fb_role && rFF[slot] == kUnsetFF) rFF[slot] = sat32(t - rA[slot]);
+      if (lane == 0 && role == ((modes >> 28) & 7u) && rFF[slot] == kUnsetFF) rFF[slot] = sat32(t - rA[slot]);
       if (P.inst[i].flags & 1u) { if (lane == (int)i) ++n_large; }
       item_done(slot);
     };
@@ -548,7 +549,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
           }
         }
       }
-      if (role == fb_role) {  // first output token at a feedback-role instance (M13)
+      if (role == ((modes >> 28) & 7u)) {  // first output token at a feedback-role instance (M13)
         // (two items of one request may both reach done == 1 in this step: the CAS lets the first set it)
         if (act && done == 1u) atomicCAS(&rFF[slot], kUnsetFF, sat32(t - rA[slot]));
         __syncwarp();
@@ -608,7 +609,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
             a = exp_sample(MI.alpha, w.x);
           }
           cost += a;
-          const uint32_t kvk = (flags >> 2) & 7u;
+          const uint32_t kvk = LV ? 0u : (flags >> 2) & 7u;   // levels >= 1 never model KV
           if (kvk) {  // M23: KV penalty of an opening RECV away from the request's KV home
             uint32_t pen;
             if (kvk == SDAS_KV_RECOMPUTE) pen = MI.beta * Pk.kv_ctx;
@@ -693,7 +694,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
           uint32_t lim = wA >> 16;                                      // out
           if (n_out > 0) lim = min(lim, wB >> 16);
           if (MAXOUT > 1 && n_out > 1) lim = min(lim, wD & 0xFFFFu);
-          sk = (role == fb_role && done == 0u) ? 1u : lim - done;
+          sk = (role == ((modes >> 28) & 7u) && done == 0u) ? 1u : lim - done;
         }
         m = __reduce_min_sync(FULL, sk);
         if (m > 1) {
@@ -794,8 +795,12 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
         }
       }
       ++jn;
-      if (jn < N) gen(jn, t);
-      else arr_near = false;
+      if (jn < N) {
+        gen(jn, t);
+      } else {
+        arr_near = false;
+        arr_more = false;
+      }
     };
 
     // ---------------------------------------------------------------- window close + control (M15, M16)
@@ -925,7 +930,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
     // ---------------------------------------------------------------- event loop (M12)
     for (;;) {
       __syncwarp();
-      if (jn >= N && nsys == 0) break;
+      if (!arr_more && nsys == 0) break;   // (arr_more == jn < N, kept in a register)
       // next tick: warp-min over 32-bit deltas (every pending event lies < 2^31 ticks ahead)
       // (branch-free: lanes that are not instances hold IDLE / empty state and contribute nothing)
       uint32_t d = st != IDLE ? end_lo - t_lo : 0xFFFFFFFFu;
@@ -948,7 +953,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
         close_window(false);
         nb_lo += W32;
         ++wk;
-        if (!arr_near && jn < N) arr_near = A_next - t < 0x80000000ull;
+        if (!arr_near && arr_more) arr_near = A_next - t < 0x80000000ull;
       }
       // phase 1 COMPLETE (instance order)
       // (lanes >= n_inst stay IDLE with empty rings: no is_inst test needed in the phase votes)
@@ -1009,7 +1014,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
         cut = true;
         do {
           arrive();
-        } while (!ovf && jn < N && arr_near && A_lo == t_lo);
+        } while (!ovf && arr_more && arr_near && A_lo == t_lo);
         if (K1_UNLIKELY(ovf)) break;
       }
       // runs cut exactly at this tick: apply their silent steps (they precede START, as in M12)
