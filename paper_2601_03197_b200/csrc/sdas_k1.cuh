@@ -61,9 +61,9 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
   const uint32_t R_cap = Pk.request_cap, n_links = Pk.n_links;
   const uint32_t W32 = (uint32_t)Pk.window;
   constexpr bool LEAN = LV >= 2;
-  const unsigned long long max_ticks = LEAN ? 0ull : Pk.max_ticks;   // LEAN grids never truncate
+  const unsigned long long max_ticks = LV ? 0ull : Pk.max_ticks;   // specialised grids never truncate
   const bool need_lint = LV == 0 && Pk.need_lint != 0;
-  const bool coalesce = LEAN || (Pk.flags & SDAS_FLAG_STEPWISE) == 0;   // silent DECODE runs
+  const bool coalesce = LV || (Pk.flags & SDAS_FLAG_STEPWISE) == 0;   // silent DECODE runs
   const bool need_pace = LV == 0 && Pk.need_pace != 0;                     // f4 M30: some link is paced
   const uint32_t key0 = (uint32_t)Pk.master_seed, key1 = (uint32_t)(Pk.master_seed >> 32);
   const unsigned long long gwarp = (unsigned long long)blockIdx.x * (blockDim.x >> 5) + wib;

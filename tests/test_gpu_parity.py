@@ -364,11 +364,11 @@ def test_lean_kernel_equals_generic(cfg):
                    n_requests=400)
     series = cfg == "config2"
     a = run_gpu(p, g, series=series)
-    assert a["res"].layout.k1_variant == (1 if cfg == "truncated_mmpp" else 2)   # LEAN never truncates
+    assert a["res"].layout.k1_variant == (0 if cfg == "truncated_mmpp" else 2)   # levels >= 1 never truncate
     b = run_gpu(p, g, series=series, generic=True)
     assert b["res"].layout.k1_variant == 0
     m = run_gpu(p, g, series=series, mid=True)
-    assert m["res"].layout.k1_variant == 1
+    assert m["res"].layout.k1_variant == (0 if cfg == "truncated_mmpp" else 1)
     _same_results(a, b, series)
     _same_results(m, b, series)
     o = oracle.simulate(p, g, series=series)
