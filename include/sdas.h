@@ -233,7 +233,7 @@ typedef struct {
   uint32_t n_instances, smem_per_replica, warps_per_block, blocks_per_sm;
   uint64_t resident_replicas;
   uint32_t k1_variant;       /* K1 specialisation level running this grid: 0 generic,
-                                1 no KV / pacing / selection / classes / LOAD metric / max_ticks / STEPWISE,
+                                1 no KV / pacing / classes / LOAD metric / max_ticks / STEPWISE,
                                 2 LEAN (+ single instances, no fan-out) */
   uint32_t pad;
 } sdas_layout;

@@ -331,14 +331,14 @@ sdas_status plan(const sdas_pipeline* p, const sdas_grid* g, Plan& pl) {
   h.max_out = 1;
   for (uint32_t r = 0; r < h.n_roles; ++r) h.max_out = std::max(h.max_out, h.role[r].n_out);
   for (uint32_t r = 0; r < h.n_roles; ++r) h.role[r].batch_words = 1 + 2 * h.max_out;
-  // K1 specialisation level: 1 = no KV modelling, no pacing, no model selection, no
-  // request classes, no LOAD-metric integral, no max_ticks truncation, no STEPWISE flag; 2 (LEAN) =
+  // K1 specialisation level: 1 = no KV modelling, no pacing, no request classes, no
+  // LOAD-metric integral, no max_ticks truncation, no STEPWISE flag; 2 (LEAN) =
   // level 1 + one instance per role (routing and snapshot JSQ are identities) and no fan-out
   h.lean = (g->flags & SDAS_FLAG_GENERIC) == 0 && !h.kv_role && !h.need_pace && !h.need_lint && !h.cls &&
            (h.flags & SDAS_FLAG_TRACE) == 0 && (g->flags & SDAS_FLAG_STEPWISE) == 0 && g->max_ticks == 0 ? 1u : 0u;
-  for (uint32_t cc = 0; cc < g->n_candidates; ++cc)
-    if (g->cand[cc].select_role >= 0) h.lean = 0;
-  if (h.lean && h.n_inst == h.n_roles && h.max_out == 1 && !(g->flags & SDAS_FLAG_MID)) h.lean = 2;
+  bool sel = false;                          // model selection needs two instances of a role: never LEAN
+  for (uint32_t cc = 0; cc < g->n_candidates; ++cc) sel = sel || g->cand[cc].select_role >= 0;
+  if (h.lean && !sel && h.n_inst == h.n_roles && h.max_out == 1 && !(g->flags & SDAS_FLAG_MID)) h.lean = 2;
 
   // --- shared-memory layout of one warp's replica
   uint64_t o = 256;  // WarpHdr

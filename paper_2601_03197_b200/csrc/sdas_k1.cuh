@@ -14,7 +14,7 @@
 // CLS (f2, M26-M29): two request classes -- per-class inbox / wait rings (class-1 ring right after the
 // class-0 ring; used only under priority service, so FIFO across classes holds otherwise), the
 // admission gate, per-class metrics.  Pipelines without interactive requests never pay for it.
-// LV: 0 generic; 1 = no KV / pacing / model selection / LOAD metric (compiled out);
+// LV: 0 generic; 1 = no KV / pacing / classes / LOAD metric / truncation (compiled out);
 // 2 (LEAN) = level 1 + one instance per role and no fan-out: routing is the identity.  Shrinks the
 // I-cache-bound hot loop.
 
@@ -883,7 +883,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
           if (TRACE) trace(TR_CONTROL, 3, 0, want ? 1u : 0u);
         }
       }
-      if (LV == 0 && cd.select_role >= 0) {  // (iii) model selection
+      if (!LEAN && cd.select_role >= 0) {  // (iii) model selection
         const DRole& Rs = P.role[cd.select_role];
         const uint32_t cs = __shfl_sync(FULL, sel_l, cd.select_role);
         const unsigned long long b1000 = (unsigned long long)__shfl_sync(FULL, acc_busy, cs) * 1000ull;

@@ -376,11 +376,14 @@ def test_lean_kernel_equals_generic(cfg):
     compare_records(a["records"], o["records"], a["summary"])
 
 
-@pytest.mark.parametrize("cfg", ["config3", "fanout_stale"])
+@pytest.mark.parametrize("cfg", ["config3", "fanout_stale", "config4_select"])
 def test_mid_kernel_equals_generic(cfg):
-    # routed pipelines without KV / pacing / selection / classes run the level-1 kernel
+    # routed / model-selecting pipelines without KV / pacing / classes / truncation run the level-1 kernel
     if cfg == "config3":
         p, g = W.config3(n_seeds=2, n_requests=250)
+    elif cfg == "config4_select":
+        cands = W.config4_candidates()
+        p, g = W.config4(n_seeds=2, n_requests=250, candidates=cands[::1024] + cands[7::1531])
     else:
         p, g = W.config3(n_seeds=2, n_requests=200)
         g["candidates"] = [W.with_stale_jsq(c, k % 3 == 0) for k, c in enumerate(g["candidates"])]
