@@ -789,7 +789,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
           ++in;
           if (coalesce) cut_run();
         }
-        if (K1_UNLIKELY(__ballot_sync(FULL, bad))) {
+        if (K1_UNLIKELY(__any_sync(FULL, bad))) {
           if (TRACE) trace(TR_OVERFLOW, 0, dest, 0);
           ovf = true;
         }
@@ -973,7 +973,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
       // phase 2 DELIVER (per destination instance, FIFO; lane = instance)
       const bool dv = fn > 0 && fhead == t_lo;
       bool cut = false;                    // a DELIVER or ARRIVE may have cut a DECODE run
-      if (__ballot_sync(FULL, dv)) {
+      if (__any_sync(FULL, dv)) {
         cut = true;
         bool lovf = false;
         if (dv) {
@@ -1002,7 +1002,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
             if (fhead != t_lo) break;
           }
         }
-        if (K1_UNLIKELY(__ballot_sync(FULL, lovf))) {
+        if (K1_UNLIKELY(__any_sync(FULL, lovf))) {
           if (TRACE) trace(TR_OVERFLOW, 0, 0, 0);
           ovf = true;
           break;
