@@ -39,10 +39,24 @@ def env_rank():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
 
 
+DEFAULT_SEEDS = {2: 2048, 3: 4096}                       # 1,048,576 replicas per GPU either way
+
+
 def workload(args, world):
+    """(pipeline, grid) of the timed workload: BASELINE config 2 (default) or config 3, weak-scaled."""
     seeds = args.seeds * world                          # weak scaling: args.seeds per GPU
-    pipe, grid = W.config2(n_seeds=seeds, n_requests=args.requests, series_stride=0)
-    return pipe, grid
+    if args.config == 3:
+        return W.config3(n_seeds=seeds, n_requests=args.requests)
+    return W.config2(n_seeds=seeds, n_requests=args.requests, series_stride=0)
+
+
+def workload_name(args):
+    if args.config == 3:
+        return ("config3: P4-chain planner->coder(2)->tester(2)->reviewer, 16 candidates (modes x RR/JSQ routing x "
+                "SLO batch control) x 16 Poisson rates x %d seeds/GPU, N=%d requests/replica" % (args.seeds,
+                                                                                                 args.requests))
+    return ("config2: P2-X dev->tester, per-1s-window mode control, 64 policies x 8 Poisson rates x %d seeds/GPU, "
+            "N=%d requests/replica" % (args.seeds, args.requests))
 
 
 def peaks():
@@ -99,7 +113,7 @@ class ClockSampler:
 def cpu_baseline(args, target_s=15.0):
     """The oracle as it stands, on this host's cores, on a bounded sample of the same workload."""
     import oracle
-    pipe, grid = W.config2(n_seeds=args.seeds, n_requests=args.requests, series_stride=0)
+    pipe, grid = workload(args, 1)
     R = W.grid_size(grid)
     threads = os.cpu_count() or 1
     probe = W.sample_ids(R, 128)
@@ -122,8 +136,8 @@ def cpu_baseline(args, target_s=15.0):
     msg1 = int(s1["arrivals"].astype(np.int64).sum() + s1["deliveries"].astype(np.int64).sum())
     return {"value": msg / dt, "unit": UNIT, "cores": threads, "kind": "oracle",
             "single_thread": {"value": msg1 / dt1, "unit": UNIT, "sample": "%d replicas" % len(ids1)},
-            "sample": "%d of %d config-2 replicas (every floor(R/n)-th id + last), N=%d requests, %.1f s" % (
-                len(ids), R, args.requests, dt),
+            "sample": "%d of %d config-%d replicas (every floor(R/n)-th id + last), N=%d requests, %.1f s" % (
+                len(ids), R, args.config, args.requests, dt),
             "replicas_per_s": len(ids) / dt, "des_events_per_s": des / dt, "seconds": dt}
 
 
@@ -132,7 +146,7 @@ def run_reference(args):
     if rank != 0:
         return
     import oracle
-    pipe, grid = W.config2(n_seeds=args.seeds, n_requests=args.requests, series_stride=0)
+    pipe, grid = workload(args, 1)
     R = W.grid_size(grid)
     threads = os.cpu_count() or 1
     per_step = args.ref_sample
@@ -151,10 +165,9 @@ def run_reference(args):
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1000 * tot_t / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-            "config": {"workload": "config2: P2-X dev->tester, 64 policies x 8 rates x %d seeds, N=%d (sampled)" % (
-                args.seeds, args.requests), "sample_per_step": per_step},
+            "config": {"workload": workload_name(args) + " (sampled)", "sample_per_step": per_step},
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "oracle",
-                             "sample": "%d replicas per step of %d (config 2)" % (per_step, R)},
+                             "sample": "%d replicas per step of %d (config %d)" % (per_step, R, args.config)},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "replicas_per_s": tot_rep / tot_t}
     print(json.dumps(line), flush=True)
@@ -166,7 +179,9 @@ def main():
     ap.add_argument("--steps", type=int, default=2)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="sdas", choices=["sdas", "reference"])
-    ap.add_argument("--seeds", type=int, default=2048, help="seeds per GPU (config 2: 2048 -> 1M replicas)")
+    ap.add_argument("--config", type=int, default=2, choices=[2, 3],
+                    help="BASELINE config timed: 2 (default, the headline) or 3 (4-agent routed DAG)")
+    ap.add_argument("--seeds", type=int, default=None, help="seeds per GPU (default: 1M replicas per GPU)")
     ap.add_argument("--requests", type=int, default=1000)
     ap.add_argument("--ref-sample", type=int, default=512)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -174,6 +189,8 @@ def main():
     ap.add_argument("--generic", action="store_true", help="A/B only: disable the K1 specialisations")
     ap.add_argument("--mid", action="store_true", help="A/B only: at most the level-1 K1 specialisation")
     args = ap.parse_args()
+    if args.seeds is None:
+        args.seeds = DEFAULT_SEEDS[args.config]
     if args.impl == "reference":
         run_reference(args)
         return
@@ -278,7 +295,8 @@ def main():
     traffic = None
     issue = None
     try:
-        prof = json.load(open(os.path.join(ROOT, "profiles", "k1_ncu_summary.json")))
+        prof = json.load(open(os.path.join(ROOT, "profiles", "k1_ncu_summary.json" if args.config == 2 else
+                                           "k1_ncu_summary_config%d.json" % args.config)))
         if prof.get("dram_bytes_per_des_event") is not None:
             traffic = prof["dram_bytes_per_des_event"] * (loc_des / args.steps)
         if prof.get("warp_instr_per_des_event") is not None:
@@ -328,8 +346,7 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-            "config": {"workload": "config2: P2-X dev->tester, per-1s-window mode control, 64 policies x 8 "
-                                   "Poisson rates x %d seeds/GPU, N=%d requests/replica" % (args.seeds, args.requests),
+            "config": {"workload": workload_name(args),
                        "replicas_per_step": reps // args.steps, "n_requests": args.requests,
                        "l2": "flushed (256 MiB write) before every step",
                        "parallelism": "replica-grid dp%d (group-interleaved), NCCL all_reduce of cells" % world},

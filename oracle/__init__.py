@@ -33,7 +33,7 @@ import subprocess
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_HERE, "liboracle.so")
+_LIB_PATH = os.environ.get("ORACLE_LIB", os.path.join(_HERE, "liboracle.so"))   # ORACLE_LIB: mutation runs only
 
 NBINS = 464
 NCNT = 28
@@ -60,6 +60,8 @@ CELL_FIELDS = ["n_replicas", "n_ok", "n_overflow", "n_truncated", "admitted", "d
 
 def build(force=False):
     src = os.path.join(_HERE, "oracle.cpp")
+    if "ORACLE_LIB" in os.environ:              # a prebuilt (mutated) oracle under test: never rebuilt here
+        return _LIB_PATH
     if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(src):
         subprocess.check_call(["g++", "-O2", "-std=c++17", "-fPIC", "-shared", "-o", _LIB_PATH, src,
                                "-lpthread"], cwd=_HERE)
@@ -167,6 +169,8 @@ def lib():
                                    C.c_uint64, C.POINTER(C.c_uint64)]
         L.orc_cells.argtypes = [C.POINTER(Grid), C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         L.orc_argmin_groups.argtypes = [C.POINTER(Grid), C.c_void_p, C.c_uint32, C.c_uint64, C.c_void_p]
+        L.orc_pooled_pct.restype = C.c_uint64
+        L.orc_pooled_pct.argtypes = [C.c_void_p, C.c_uint32]
         L.orc_argmin_rows.argtypes = [C.POINTER(Grid), C.c_void_p, C.c_void_p, C.c_uint32, C.c_uint64,
                                       C.c_void_p]
         _lib = L
@@ -321,6 +325,12 @@ def argmin_rows(pipe, grid, cnt, hist, objective="p99_e2e", slo=0):
     lib().orc_argmin_rows(C.byref(p.grid), np.ascontiguousarray(cnt).ctypes.data,
                           np.ascontiguousarray(hist).ctypes.data, OBJECTIVES[objective], slo, best.ctypes.data)
     return best
+
+
+def pooled_pct(hist, num):
+    """M18 on one pooled histogram (NBINS counts): lower edge of the num-th percentile's bin."""
+    h = np.ascontiguousarray(np.asarray(hist, dtype=np.int64))
+    return lib().orc_pooled_pct(h.ctypes.data, num)
 
 
 # ------------------------------------------------------------------ primitives

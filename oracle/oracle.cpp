@@ -371,7 +371,8 @@ struct Replica {
     uint64_t ffl = ff[j] - A[j];
     uint32_t e32 = e2e > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)e2e;
     uint32_t f32 = ffl > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)ffl;
-    // saturated iff a field reaches 2^32-1 (reading R-SAT); sum_ff sums saturated values
+    // a record field saturates at 2^32-1 (M18); a record holding the sentinel counts as saturated
+    // (reading R-SAT).  The sums stay exact u64 (M19: "sum e2e, sum ff (u64)").
     if (e2e >= 0xFFFFFFFFull || ffl >= 0xFFFFFFFFull) S.n_saturated++;
     if (rec) { rec[2 * S.completed] = e32; rec[2 * S.completed + 1] = f32; }
     hist[bin_of(e32)]++;
@@ -385,7 +386,7 @@ struct Replica {
     }
     S.completed++;
     S.sum_e2e += e2e;
-    S.sum_ff += f32;
+    S.sum_ff += ffl;
     S.max_e2e = std::max(S.max_e2e, e32);
     if (e2e <= P.slo) S.good++;
     w_n++;
@@ -996,7 +997,12 @@ struct Key {
   uint64_t dropped, p, sum, completed, makespan, good, large;
   uint32_t c;
 };
-bool rate_gt(uint64_t na, uint64_t ma, uint64_t nb, uint64_t mb) { return (u128)na * mb > (u128)nb * ma; }
+// na/ma > nb/mb; a zero makespan is rate 0 (reading R-RATE0), which keeps the order total
+bool rate_gt(uint64_t na, uint64_t ma, uint64_t nb, uint64_t mb) {
+  if (ma == 0) { na = 0; ma = 1; }
+  if (mb == 0) { nb = 0; mb = 1; }
+  return (u128)na * mb > (u128)nb * ma;
+}
 bool better(const Key& a, const Key& b, uint32_t obj, uint64_t slo) {
   if (a.bad != b.bad) return a.bad < b.bad;
   switch (obj) {
@@ -1032,9 +1038,26 @@ bool better(const Key& a, const Key& b, uint32_t obj, uint64_t slo) {
   }
   return a.c < b.c;
 }
+
+// M18 on a pooled cell histogram: the lower edge of the bin holding the nearest-rank num-th percentile
+// (the first bin whose cumulative count reaches ceil(num n / 100)); UINT32_MAX for an empty histogram.
+uint64_t pooled_pct(const int64_t* h, uint32_t num) {
+  uint64_t n = 0;
+  for (int b = 0; b < ORC_NBINS; ++b) n += (uint64_t)h[b];
+  if (n == 0) return 0xFFFFFFFFull;
+  const uint64_t k = (num * n + 99) / 100;
+  uint64_t cum = 0;
+  for (uint32_t b = 0; b < ORC_NBINS; ++b) {
+    cum += (uint64_t)h[b];
+    if (cum >= k) return bin_lo(b);
+  }
+  return 0xFFFFFFFFull;
+}
 }  // namespace
 
 extern "C" {
+
+uint64_t orc_pooled_pct(const int64_t* hist, uint32_t num) { return pooled_pct(hist, num); }
 
 void orc_argmin_groups(const orc_grid* g, const orc_summary* sums, uint32_t obj, uint64_t slo, int32_t* best) {
   uint64_t C = g->n_cand;
@@ -1070,17 +1093,7 @@ void orc_argmin_rows(const orc_grid* g, const int64_t* cnt, const int64_t* hist,
       const int64_t* q = cnt + cell * ORC_NCNT;
       const int64_t* h = hist + cell * ORC_NHIST * ORC_NBINS +
                          (obj == ORC_OBJ_P99_FF ? ORC_NBINS : obj == ORC_OBJ_P99_E2E_INT ? 2 * ORC_NBINS : 0);
-      uint64_t n = 0;
-      for (int b = 0; b < ORC_NBINS; ++b) n += (uint64_t)h[b];
-      uint64_t p = 0xFFFFFFFFull;
-      if (n > 0) {
-        uint32_t num = obj == ORC_OBJ_P50_E2E ? 50 : obj == ORC_OBJ_P90_E2E ? 90 : 99;
-        uint64_t k = (num * n + 99) / 100, cum = 0;
-        for (uint32_t b = 0; b < ORC_NBINS; ++b) {
-          cum += (uint64_t)h[b];
-          if (cum >= k) { p = bin_lo(b); break; }
-        }
-      }
+      const uint64_t p = pooled_pct(h, obj == ORC_OBJ_P50_E2E ? 50 : obj == ORC_OBJ_P90_E2E ? 90 : 99);
       Key k{};
       k.bad = q[1] != q[0];
       k.dropped = (uint64_t)q[5];

@@ -153,6 +153,8 @@ void orc_cells(const orc_grid* g, const orc_summary* sums, const uint32_t* hists
 /* Per-group argmin (M20): best[g] = winning candidate c; per-row argmin over pooled cells. */
 void orc_argmin_groups(const orc_grid* g, const orc_summary* sums, uint32_t objective,
                        uint64_t obj_slo, int32_t* best);
+/* M18 on a pooled histogram [ORC_NBINS]: lower edge of the nearest-rank num-th percentile's bin */
+uint64_t orc_pooled_pct(const int64_t* hist, uint32_t num);
 void orc_argmin_rows(const orc_grid* g, const int64_t* cnt, const int64_t* hist,
                      uint32_t objective, uint64_t obj_slo, int32_t* best);
 

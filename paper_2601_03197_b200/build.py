@@ -7,7 +7,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.environ.get("SDAS_LIB", os.path.join(HERE, "libsdas.so"))   # SDAS_LIB: alternate build (debug)
 SOURCES = [os.path.join(CSRC, "sdas_kernels.cu"), os.path.join(CSRC, "sdas_host.cpp")]
-HEADERS = [os.path.join(CSRC, "sdas_internal.h"), os.path.join(os.path.dirname(HERE), "include", "sdas.h")]
+HEADERS = [os.path.join(CSRC, f) for f in sorted(os.listdir(CSRC)) if f.endswith((".h", ".cuh"))] + \
+    [os.path.join(os.path.dirname(HERE), "include", "sdas.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
          "-Xcompiler", "-fPIC", "-shared"]

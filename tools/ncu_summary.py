@@ -1,5 +1,5 @@
 """Summarise a K1 `ncu --set full` capture (tools/profile_k1.py) into profiles/<dir>/k1_ncu_summary.json.
-usage: python tools/ncu_summary.py <report.ncu-rep> <profile_k1 log> <out.json>"""
+usage: python tools/ncu_summary.py <report.ncu-rep> <profile_k1 log> <out.json> [config label]"""
 import csv
 import io
 import json
@@ -22,7 +22,8 @@ d = {k: v[h.index(k)] for k in keys if k in h}
 d["units"] = {k: u[h.index(k)] for k in keys if k in h}
 m = re.search(r"replicas (\d+) des_events (\d+) msg_events (\d+)", open(log).read())
 R, des = int(m.group(1)), int(m.group(2))
-d["workload"] = "tools/profile_k1.py: config-2 grid, %d replicas x 1000 requests, %d DES events (1 launch)" % (R, des)
+cfg = sys.argv[4] if len(sys.argv) > 4 else "config-2"
+d["workload"] = "tools/profile_k1.py: " + cfg + " grid, %d replicas x 1000 requests, %d DES events (1 launch)" % (R, des)
 d["warp_instr_per_des_event"] = float(d["smsp__inst_executed.sum"]) / des
 scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 dram = sum(float(d[k]) * scale[d["units"][k]] for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))

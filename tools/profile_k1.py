@@ -18,6 +18,8 @@ if a.config == 2:
     pipe, grid = W.config2(n_seeds=a.seeds, n_requests=a.requests, series_stride=0)
 elif a.config == 1:
     pipe, grid = W.config1(n_seeds=a.seeds, n_requests=a.requests)
+elif a.config == 3:
+    pipe, grid = W.config3(n_seeds=a.seeds, n_requests=a.requests)
 P = sdas.Pipeline(pipe)
 gv = sdas.GridView(pipe, grid)
 r = sdas.control_sweep(P, gv, objective="p99_e2e")
