@@ -80,7 +80,7 @@ enum { SDAS_SCOPE_REPLICA = 0, SDAS_SCOPE_CELL = 1, SDAS_SCOPE_GROUP = 2, SDAS_S
 #define SDAS_NBINS 464       /* rule M17: log-linear bins over u32 latencies */
 #define SDAS_NCNT 28         /* int64 counters per cell */
 #define SDAS_NHIST 3         /* histograms per cell: e2e, first feedback, interactive e2e (M29) */
-#define SDAS_SUMMARY_BYTES 160
+#define SDAS_SUMMARY_BYTES 176
 
 /* ---- pipeline description ---------- */
 typedef struct {           /* per-message and per-token service model of one agent instance */
@@ -141,7 +141,7 @@ void sdas_pipeline_destroy(sdas_pipeline* p); /* NULL-safe */
 /* Table 1: set(parameter, value) / reset(parameter) on the pipeline's
  * knob registry ("each agent exposes ... knobs").  Knobs (SPEC.md:209, 498 addressing):
  *   "agent:<role>/max_num_seqs"      1..32      (default: desc value)
- *   "agent:<role>/n_functions"       1..65535
+ *   "agent:<role>/n_functions"       1..255
  *   "link:<src>-><dst>/comm_mode"    0..2       (SDAS_BATCH/FUNCTION/TOKEN)
  *   "link:<src>-><dst>/chunk_tokens" 1..65535
  *   "link:<src>-><dst>/net_delay"    1..2^31-1
@@ -211,15 +211,17 @@ typedef struct {
 typedef struct {
   uint64_t params_bytes;     /* device: packed descriptors (written by the library) */
   uint64_t work_bytes;       /* device: scratch (replica counter + per-warp record scratch) */
-  uint64_t summary_bytes;    /* device: n_local_replicas x 160-byte summary records, little-endian u32 words:
+  uint64_t summary_bytes;    /* device: n_local_replicas x 176-byte summary records, little-endian u32 words:
                                 0 status, 1 admitted, 2 dropped, 3 completed, 4-5 makespan (or overflow tick),
                                 6-7 sum e2e, 8-9 sum ff, 10-11 integral N_sys dt, 12-15 p50/p99 e2e, p50/p99 ff,
                                 16 bins of p50/p99 e2e (u16 pair), 17 exact p90 e2e (f3), 18 max e2e, 19 saturated records, 20 arrivals,
                                 21 deliveries, 22 RECV steps, 23 DECODE steps, 24 window closes, 25 mode
-                                switches, 26 good, 27 large-model items, 28-29 output tokens, 30 batch|select
-                                changes (u16 pair), 31 KV transfers (M24); f2 (M29): 32 interactive
+                                switches, 26 good, 27 large-model items, 28-29 output tokens, 30 max_num_seqs
+                                changes (M16(ii)), 31 KV transfers (M24); f2 (M29): 32 interactive
                                 completions, 33 rejected by the admission gate, 34-35 sum interactive e2e,
-                                36-37 exact p50/p99 interactive e2e, 38 interactive good, 39 gate changes */
+                                36-37 exact p50/p99 interactive e2e, 38 interactive good, 39 gate changes;
+                                40 model-selection changes (M16(iii)), 41 bins of p50/p99 ff (u16 pair),
+                                42-43 reserved (0).  Sums are exact u64; latencies saturate at 2^32-1 */
   uint64_t records_bytes;    /* device: n_local_replicas x n_requests x {u32 e2e, u32 ff} (FLAG_RECORDS) */
   uint64_t series_bytes;     /* device: series_slots x series_windows x n_instances x 16 B (FLAG_SERIES);
                                 zeroed by sdas_simulate: windows a replica never reaches (it ended or

@@ -70,12 +70,8 @@ struct sdas_pipeline {
 
 namespace {
 
-uint32_t host_bin(uint32_t v) {   // rule M17 bin of an exact percentile (0xFFFF when there is none)
-  if (v == 0xFFFFFFFFu) return 0xFFFFu;
-  if (v < 16u) return v;
-  uint32_t e = 31u - (uint32_t)__builtin_clz(v);
-  return 16u + 16u * (e - 4u) + ((v >> (e - 4u)) & 15u);
-}
+// Largest value EXP(M; x) can return (x = 0, rule M3): floor(M * round(2^32 ln 2) * 32 / 2^32) <= 22.19 M.
+uint64_t exp_max(uint64_t M) { return (uint64_t)(((unsigned __int128)M * 2977044472ull * 32u) >> 32) + 1; }
 
 sdas_status validate_desc(const sdas_pipeline_desc* d) {
   if (!d) return fail(SDAS_E_INVALID_ARG, "desc is NULL");
@@ -116,6 +112,17 @@ sdas_status validate_desc(const sdas_pipeline_desc* d) {
       if (c.h_msg >= (1u << 31) || c.alpha >= (1u << 31) || c.beta >= (1u << 15) || c.tau0 >= (1u << 31) ||
           c.gamma >= (1u << 25))
         return fail(SDAS_E_INVALID_FIELD, "roles[%u].cost: step costs must stay below 2^31 ticks", r);
+      // worst-case step costs (K1 keeps every pending tick < 2^31 ahead): RECV of a 65535-token
+      // message with the largest EXP draw (M3 tail) and the largest KV penalty (M23); DECODE of 32 sequences
+      const uint64_t a_max = R.svc == SDAS_SVC_EXP ? exp_max(c.alpha) : c.alpha;
+      uint64_t pen = 0;
+      if (d->kv_role && r == d->kv_role)
+        pen = std::max<uint64_t>((uint64_t)c.beta * d->kv_ctx_tokens, (uint64_t)d->kv_tau_xfer * d->kv_ctx_tokens);
+      if ((uint64_t)c.h_msg + (uint64_t)c.beta * 65535u + a_max + pen >= (1ull << 31))
+        return fail(SDAS_E_INVALID_FIELD, "roles[%u].cost: worst-case RECV (h + 65535 beta + max alpha draw + KV "
+                                          "penalty) must stay below 2^31 ticks", r);
+      if ((uint64_t)c.tau0 + (uint64_t)c.gamma * SDAS_MAX_BATCH >= (1ull << 31))
+        return fail(SDAS_E_INVALID_FIELD, "roles[%u].cost: tau0 + 32 gamma must stay below 2^31 ticks", r);
     }
   }
   if (n_inst > SDAS_MAX_INSTANCES) return fail(SDAS_E_LIMIT, "instances: at most %d in total", SDAS_MAX_INSTANCES);
@@ -313,9 +320,11 @@ sdas_status plan(const sdas_pipeline* p, const sdas_grid* g, Plan& pl) {
         return fail(SDAS_E_INVALID_FIELD, "cand[%u].pacing_gap x flight_cap must stay below 2^30", cc);
     if (pg) h.need_pace = 1;
   }
-  h.cls = 0;
+  h.cls = 0;   // the CLS instantiation runs request classes (M26-M29) and the admission gate (M28)
   for (uint64_t a = 0; a < (uint64_t)g->n_rates * g->n_profiles; ++a)
     if (g->arrivals[a].interactive_permille) h.cls = 1;
+  for (uint32_t cc = 0; cc < g->n_candidates; ++cc)
+    if (g->cand[cc].admit) h.cls = 1;   // a gate with one class rejects every arrival while closed
   h.kv_ctx = p->kv_ctx;
   h.kv_tau = p->kv_tau;
   h.kv_skew32 = ((uint64_t)p->kv_skew << 32) / 1000;
@@ -344,7 +353,7 @@ sdas_status plan(const sdas_pipeline* p, const sdas_grid* g, Plan& pl) {
   uint64_t o = 256;  // WarpHdr
   const uint32_t R = p->request_cap;
   h.off_reqA = (uint32_t)o; o += 8ull * R;
-  h.off_reqFF = (uint32_t)o; o += 4ull * R;
+  h.off_reqFF = (uint32_t)o; o += 8ull * R;              // exact u64 first-feedback latency (M13, M19)
   h.off_reqJ = (uint32_t)o; o += 4ull * R;
   h.off_reqO = (uint32_t)o; o += 4ull * R;
   h.off_reqNit = (uint32_t)o; o += 2ull * R;
@@ -755,7 +764,7 @@ sdas_status sdas_metrics(const sdas_pipeline* p, const sdas_grid* grid, const sd
     out->makespan = u64(4); out->sum_e2e = u64(6); out->sum_ff = u64(8); out->int_nsys = u64(10);
     out->p50_e2e = w[12]; out->p99_e2e = w[13]; out->p50_ff = w[14]; out->p99_ff = w[15];
     out->bin_p50_e2e = w[16] & 0xFFFF; out->bin_p99_e2e = w[16] >> 16;
-    out->bin_p50_ff = host_bin(w[14]); out->bin_p99_ff = host_bin(w[15]);   // derivable: not stored
+    out->bin_p50_ff = w[41] & 0xFFFF; out->bin_p99_ff = w[41] >> 16;
     out->p90_e2e = w[17];
     out->arrivals = w[20]; out->deliveries = w[21]; out->recv_steps = w[22]; out->decode_steps = w[23];
     out->window_closes = w[24]; out->mode_switches = w[25]; out->good = w[26]; out->large_items = w[27];
@@ -779,7 +788,7 @@ sdas_status sdas_metrics(const sdas_pipeline* p, const sdas_grid* grid, const sd
     if (index >= pl.n_cells) return fail(SDAS_E_INVALID_ARG, "index out of range");
     const int64_t* q = reinterpret_cast<const int64_t*>(host->cell_cnt) + index * SDAS_NCNT;
     const int32_t* h = reinterpret_cast<const int32_t*>(host->cell_hist) + index * SDAS_NHIST * SDAS_NBINS;
-    out->status = q[1] == q[0] ? SDAS_REPLICA_OK : SDAS_REPLICA_OVERFLOW;
+    out->status = q[2] ? SDAS_REPLICA_OVERFLOW : q[3] ? SDAS_REPLICA_TRUNCATED : SDAS_REPLICA_OK;
     out->n_replicas = q[0]; out->admitted = q[4]; out->dropped = q[5]; out->completed = q[6];
     out->sum_e2e = q[7]; out->sum_ff = q[8]; out->makespan = q[9]; out->int_nsys = q[10]; out->good = q[11];
     out->large_items = q[12]; out->arrivals = q[13]; out->deliveries = q[14]; out->recv_steps = q[15];

@@ -9,9 +9,9 @@
 
 namespace sdas {
 
-constexpr uint32_t kUnsetFF = 0xFFFFFFFFu;   // ff latency not yet observed (also "saturated")
+constexpr unsigned long long kUnsetFF = ~0ull;   // first-feedback latency not yet observed (u64 slot)
 constexpr uint32_t kNever = 0xFFFFFFFFu;
-constexpr int kScratchMin = SDAS_NHIST * SDAS_NBINS * 4 + 256 * 4 + 160 + SDAS_NCNT * 8;  // finalize scratch
+constexpr int kScratchMin = SDAS_NHIST * SDAS_NBINS * 4 + 256 * 4 + SDAS_SUMMARY_BYTES + SDAS_NCNT * 8;  // finalize scratch
 
 struct DInst {          // one instance, 64 B
   uint32_t role, h, alpha, beta, tau0, gamma, B_default, flags;   // flags: bit0 large, bit1 svc_exp

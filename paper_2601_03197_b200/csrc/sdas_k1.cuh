@@ -48,7 +48,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
   uint8_t* const Wr = smem + Pk.off_warps + wib * Pk.smem_per_warp;
   WarpHdr* const H = reinterpret_cast<WarpHdr*>(Wr);
   unsigned long long* const rA = at<unsigned long long>(Wr, Pk.off_reqA);
-  uint32_t* const rFF = at<uint32_t>(Wr, Pk.off_reqFF);
+  unsigned long long* const rFF = at<unsigned long long>(Wr, Pk.off_reqFF);
   uint32_t* const rJ = at<uint32_t>(Wr, Pk.off_reqJ);
   uint32_t* const rO = at<uint32_t>(Wr, Pk.off_reqO);
   uint16_t* const rNit = at<uint16_t>(Wr, Pk.off_reqNit);
@@ -309,11 +309,10 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
     auto request_complete = [&](uint32_t slot) {
       --nsys;
       if (lane == 0) {                     // counters and the record: lane 0 owns them
-        const unsigned long long e2e = t - rA[slot];
-        const uint32_t f32 = rFF[slot];
-        const uint32_t e32 = sat32(e2e);
+        const unsigned long long e2e = t - rA[slot], ff = rFF[slot];
+        const uint32_t f32 = sat32(ff), e32 = sat32(e2e);
         WarpHdr& h = *H;
-        if (e2e >= 0xFFFFFFFFull || f32 == 0xFFFFFFFFu) ++h.n_sat;
+        if (e2e >= 0xFFFFFFFFull || ff >= 0xFFFFFFFFull) ++h.n_sat;   // a field holds the sentinel (R-SAT)
         rec[h.completed] = (unsigned long long)e32 | ((unsigned long long)f32 << 32);
         if (CLS) {                         // M29 per-class metrics
           const uint32_t ci = rCls[slot];
@@ -326,7 +325,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
         }
         ++h.completed;
         h.sum_e2e += e2e;
-        h.sum_ff += f32;
+        h.sum_ff += ff;                    // exact (M19)
         h.max_e2e = max(h.max_e2e, e32);
         h.good += e2e <= Pk.slo ? 1u : 0u;
         ++h.w_n;
@@ -403,7 +402,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
         if (K1_UNLIKELY(ovf)) return;
       }
       __syncwarp();                        // lane 0's ring writes precede the destinations' DELIVER reads
-      if (lane == 0 && role == ((modes >> 28) & 7u) && rFF[slot] == kUnsetFF) rFF[slot] = sat32(t - rA[slot]);
+      if (lane == 0 && role == ((modes >> 28) & 7u) && rFF[slot] == kUnsetFF) rFF[slot] = t - rA[slot];
       if (P.inst[i].flags & 1u) { if (lane == (int)i) ++n_large; }
       item_done(slot);
     };
@@ -551,7 +550,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
       }
       if (role == ((modes >> 28) & 7u)) {  // first output token at a feedback-role instance (M13)
         // (two items of one request may both reach done == 1 in this step: the CAS lets the first set it)
-        if (act && done == 1u) atomicCAS(&rFF[slot], kUnsetFF, sat32(t - rA[slot]));
+        if (act && done == 1u) atomicCAS(&rFF[slot], kUnsetFF, t - rA[slot]);
         __syncwarp();
       }
       const uint32_t fin = __ballot_sync(FULL, act && done == out);
@@ -611,9 +610,9 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
           cost += a;
           const uint32_t kvk = LV ? 0u : (flags >> 2) & 7u;   // levels >= 1 never model KV
           if (kvk) {  // M23: KV penalty of an opening RECV away from the request's KV home
-            uint32_t pen;
-            if (kvk == SDAS_KV_RECOMPUTE) pen = MI.beta * Pk.kv_ctx;
-            else if (kvk == SDAS_KV_POSTHOC) pen = Pk.kv_tau * Pk.kv_ctx;
+            unsigned long long pen;
+            if (kvk == SDAS_KV_RECOMPUTE) pen = (unsigned long long)MI.beta * Pk.kv_ctx;
+            else if (kvk == SDAS_KV_POSTHOC) pen = (unsigned long long)Pk.kv_tau * Pk.kv_ctx;
             else pen = (uint32_t)max(0, (int32_t)(my_iready[ih] - t_lo));
             cost += pen;
             ++cnt_kv;
@@ -1057,12 +1056,12 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
     uint8_t* const sum_out = summary + x * SDAS_SUMMARY_BYTES;
     const unsigned long long rid = g * C + c;
     const unsigned long long cell = ((g / Pk.S) % (Pk.I * (unsigned long long)Pk.K)) * C + c;
-    uint32_t* const stg = scratch + SDAS_NHIST * SDAS_NBINS + 256;   // 40 summary words, then counters
-    unsigned long long* const cst = reinterpret_cast<unsigned long long*>(stg + 40);
+    uint32_t* const stg = scratch + SDAS_NHIST * SDAS_NBINS + 256;   // 44 summary words, then counters
+    unsigned long long* const cst = reinterpret_cast<unsigned long long*>(stg + SDAS_SUMMARY_BYTES / 4);
     __syncwarp();
     if (ovf) {
       stg[lane] = 0;
-      if (lane < 8) stg[32 + lane] = 0;
+      if (lane < SDAS_SUMMARY_BYTES / 4 - 32) stg[32 + lane] = 0;
       __syncwarp();
       if (lane == 0) {
         stg[0] = SDAS_REPLICA_OVERFLOW;
@@ -1071,6 +1070,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
         stg[12] = stg[13] = stg[14] = stg[15] = 0xFFFFFFFFu;
         stg[16] = stg[17] = 0xFFFFFFFFu;
         stg[36] = stg[37] = 0xFFFFFFFFu;
+        stg[41] = 0xFFFFFFFFu;
       }
       __syncwarp();
       if (lane < SDAS_SUMMARY_BYTES / 16)
@@ -1191,11 +1191,12 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
       stg[20] = arrivals; stg[21] = deliv; stg[22] = recvs; stg[23] = decs;
       stg[24] = window_closes; stg[25] = mode_switches; stg[26] = good; stg[27] = larges;
       stg[28] = (uint32_t)tokens; stg[29] = (uint32_t)(tokens >> 32);
-      stg[30] = (batch_changes & 0xFFFFu) | (select_changes << 16);
+      stg[30] = batch_changes;
       stg[31] = kvs;
       stg[32] = h.completed_int; stg[33] = h.rejected;
       stg[34] = (uint32_t)h.sum_e2e_int; stg[35] = (uint32_t)(h.sum_e2e_int >> 32);
       stg[36] = v50i; stg[37] = v99i; stg[38] = h.good_int; stg[39] = h.gate_changes;
+      stg[40] = select_changes; stg[41] = b50f | (b99f << 16); stg[42] = 0; stg[43] = 0;
       cst[24] = h.completed_int; cst[25] = h.rejected; cst[26] = h.sum_e2e_int; cst[27] = h.good_int;
       cst[0] = 1; cst[1] = status == SDAS_REPLICA_OK; cst[2] = 0; cst[3] = status == SDAS_REPLICA_TRUNCATED;
       cst[4] = admitted; cst[5] = dropped; cst[6] = completed; cst[7] = sum_e2e; cst[8] = sum_ff;

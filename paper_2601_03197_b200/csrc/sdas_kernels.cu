@@ -7,7 +7,7 @@
 //                    ballot/popc emission and compaction, in-loop window metrics + controller
 //                    (PAPER.md:18, 58-63, 196-220, 231-238, 278-280), and a finalize that builds
 //                    log-bin histograms in shared memory, selects exact nearest-rank p50/p99 from
-//                    the L2-resident records by radix select, writes the 128-B summary with
+//                    the L2-resident records by radix select, writes the 176-B summary with
 //                    vector stores and merges histograms/counters into cells with integer atomics.
 // K3 k3_group_argmin: per group (all C candidates of one (i,k,s)) lexicographic argmin (M20).
 // K4 k4_cell_pct    : pooled cell percentile (lower bin edge) for the row objective.
@@ -147,7 +147,9 @@ struct Key {
 
 __device__ __forceinline__ bool rate_gt(unsigned long long na, unsigned long long ma, unsigned long long nb,
                                         unsigned long long mb) {
-  // na/ma > nb/mb  <=>  na*mb > nb*ma, compared as 128-bit products
+  // na/ma > nb/mb  <=>  na*mb > nb*ma, compared as 128-bit products; a zero makespan is rate 0 (R-RATE0)
+  if (ma == 0) { na = 0; ma = 1; }
+  if (mb == 0) { nb = 0; mb = 1; }
   const unsigned long long h1 = __umul64hi(na, mb), l1 = na * mb;
   const unsigned long long h2 = __umul64hi(nb, ma), l2 = nb * ma;
   return h1 != h2 ? h1 > h2 : l1 > l2;

@@ -20,14 +20,30 @@ def local_group_ids(n_groups, rank, world, group_range=None):
     return np.arange(first, ge, world, dtype=np.int64)
 
 
+def _staged(group):
+    """gloo (the CPU test backend, or several ranks sharing one GPU) collects host tensors; NCCL device ones."""
+    import torch.distributed as dist
+    return dist.get_backend(group) == "gloo"
+
+
+def _all_reduce_sum(x, group):
+    import torch.distributed as dist
+    if _staged(group) and x.is_cuda:
+        h = x.cpu()
+        dist.all_reduce(h, op=dist.ReduceOp.SUM, group=group)
+        x.copy_(h)
+    else:
+        dist.all_reduce(x, op=dist.ReduceOp.SUM, group=group)
+
+
 def reduce_cells(result, group=None):
     """all_reduce(SUM) of the int64 counters and int32 histograms of every cell (in place)."""
-    import torch.distributed as dist
+    import torch
     L = result.layout
-    cnt = result.t["cell_cnt"][: L.n_cells * sdas.NCNT * 8].view(dtype=__import__("torch").int64)
-    hist = result.t["cell_hist"][: L.n_cells * sdas.NHIST * sdas.NBINS * 4].view(dtype=__import__("torch").int32)
-    dist.all_reduce(cnt, op=dist.ReduceOp.SUM, group=group)
-    dist.all_reduce(hist, op=dist.ReduceOp.SUM, group=group)
+    cnt = result.t["cell_cnt"][: L.n_cells * sdas.NCNT * 8].view(dtype=torch.int64)
+    hist = result.t["cell_hist"][: L.n_cells * sdas.NHIST * sdas.NBINS * 4].view(dtype=torch.int32)
+    _all_reduce_sum(cnt, group)
+    _all_reduce_sum(hist, group)
 
 
 def gather_best_groups(result, n_groups, rank, world, group=None):
@@ -40,11 +56,15 @@ def gather_best_groups(result, n_groups, rank, world, group=None):
     n = L.n_local_groups
     if n:
         mine[:n] = result.t["best_group"][: n * 4].view(torch.int32)
+    dev = mine.device
+    if _staged(group) and mine.is_cuda:
+        mine = mine.cpu()
     out = [torch.empty_like(mine) for _ in range(world)]
     dist.all_gather(out, mine, group=group)
-    table = torch.empty(n_groups, dtype=torch.int32, device=mine.device)
+    out = [o.to(dev) for o in out]
+    table = torch.empty(n_groups, dtype=torch.int32, device=dev)
     for r in range(world):
-        ids = torch.as_tensor(local_group_ids(n_groups, r, world), device=mine.device)
+        ids = torch.as_tensor(local_group_ids(n_groups, r, world), device=dev)
         table[ids] = out[r][: len(ids)]
     return table
 

@@ -46,10 +46,11 @@ SUMMARY_DTYPE = np.dtype([
     ("bin_p50_e2e", "<u2"), ("bin_p99_e2e", "<u2"), ("p90_e2e", "<u4"), ("max_e2e", "<u4"), ("n_saturated", "<u4"),
     ("arrivals", "<u4"), ("deliveries", "<u4"), ("recv_steps", "<u4"), ("decode_steps", "<u4"),
     ("window_closes", "<u4"), ("mode_switches", "<u4"), ("good", "<u4"), ("large_items", "<u4"),
-    ("tokens", "<u8"), ("batch_changes", "<u2"), ("select_changes", "<u2"), ("kv_transfers", "<u4"),
+    ("tokens", "<u8"), ("batch_changes", "<u4"), ("kv_transfers", "<u4"),
     ("completed_int", "<u4"), ("rejected", "<u4"), ("sum_e2e_int", "<u8"), ("p50_e2e_int", "<u4"),
-    ("p99_e2e_int", "<u4"), ("good_int", "<u4"), ("gate_changes", "<u4")])
-assert SUMMARY_DTYPE.itemsize == 160
+    ("p99_e2e_int", "<u4"), ("good_int", "<u4"), ("gate_changes", "<u4"), ("select_changes", "<u4"),
+    ("bin_p50_ff", "<u2"), ("bin_p99_ff", "<u2"), ("reserved", "<u4", (2,))])
+assert SUMMARY_DTYPE.itemsize == 176
 SERIES_DTYPE = np.dtype([("qint", "<u8"), ("busy", "<u4"), ("maxq", "<u2"), ("mode", "u1"), ("B", "u1")])
 TRACE_DTYPE = np.dtype([("tick", "<u8"), ("code", "<u4"), ("a", "<u4"), ("b", "<u4"), ("c", "<u4")])
 CELL_FIELDS = ["n_replicas", "n_ok", "n_overflow", "n_truncated", "admitted", "dropped", "completed",
@@ -420,17 +421,40 @@ class Result:
         return raw[8: 8 + 24 * min(n, cap)].view(TRACE_DTYPE)
 
 
-def allocate(layout, device, flags):
-    import torch
-    need = {"params": layout.params_bytes, "work": layout.work_bytes, "summary": layout.summary_bytes,
+def _needs(layout, flags):
+    """Byte size of every buffer a call with `flags` writes (sdas_results_layout)."""
+    return {"params": layout.params_bytes, "work": layout.work_bytes, "summary": layout.summary_bytes,
             "records": layout.records_bytes if flags & FLAG_RECORDS else 0,
             "series": layout.series_bytes if flags & FLAG_SERIES else 0,
+            "cell_cnt": layout.cell_cnt_bytes, "cell_hist": layout.cell_hist_bytes,
             "best_group": layout.best_group_bytes, "best_row": layout.best_row_bytes,
             "trace": layout.trace_bytes if flags & FLAG_TRACE else 0}
-    t = {k: torch.empty(int(v), dtype=torch.uint8, device=device) for k, v in need.items() if v}
+
+
+def allocate(layout, device, flags):
+    import torch
+    need = _needs(layout, flags)
+    t = {k: torch.empty(int(v), dtype=torch.uint8, device=device) for k, v in need.items()
+         if v and k not in ("cell_cnt", "cell_hist")}
     t["cell_cnt"] = torch.zeros(int(layout.cell_cnt_bytes), dtype=torch.uint8, device=device)
     t["cell_hist"] = torch.zeros(int(layout.cell_hist_bytes), dtype=torch.uint8, device=device)
     return t
+
+
+def check_buffers(result, layout, flags, device):
+    """A reused Result must hold every buffer the new layout needs, large enough, on `device`: the C-ABI
+    carries no buffer sizes, so a smaller buffer would let the kernels write out of bounds."""
+    import torch
+    dev = torch.device(device)
+    for name, nbytes in _needs(layout, flags).items():
+        if not nbytes:
+            continue
+        x = result.t.get(name)
+        if x is None or x.numel() < nbytes:
+            raise SdasError(E_BUFFER, "result buffer '%s' holds %d bytes, the grid needs %d"
+                            % (name, 0 if x is None else x.numel(), nbytes))
+        if x.device.type != dev.type or (dev.index is not None and x.device.index != dev.index):
+            raise SdasError(E_BUFFER, "result buffer '%s' is on %s, the call runs on %s" % (name, x.device, dev))
 
 
 def _stream(device):
@@ -447,6 +471,7 @@ def simulate(pipeline, gv, device="cuda", result=None, objective=None, objective
     if result is None:
         result = Result(L, allocate(L, device, gv.flags))
     else:
+        check_buffers(result, L, gv.flags, device)
         result.layout = L
     bufs = result.buffers()
     if objective is None:

@@ -10,7 +10,7 @@ FIELDS = ["status", "admitted", "dropped", "completed", "sum_e2e", "sum_ff", "in
           "window_closes", "mode_switches", "good", "large_items", "tokens", "batch_changes", "select_changes",
           "kv_transfers", "p90_e2e", "completed_int", "rejected", "sum_e2e_int", "p50_e2e_int", "p99_e2e_int",
           "good_int", "gate_changes"]
-BINS = ["bin_p50_e2e", "bin_p99_e2e"]
+BINS = ["bin_p50_e2e", "bin_p99_e2e", "bin_p50_ff", "bin_p99_ff"]
 
 
 def run_gpu(pipe, grid, records=True, series=False, trace_replica=None, objective=None, objective_slo=0,

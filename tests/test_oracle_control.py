@@ -315,3 +315,29 @@ def test_saturated_latencies(orc):
     assert int(s["sum_e2e"]) == 10 * s_ and int(s["sum_ff"]) == 10 * s_          # exact u64 sums (M19)
     assert int(s["max_e2e"]) == sat and int(s["p99_e2e"]) == sat and int(s["p50_e2e"]) == 2 * s_
     assert int(s["bin_p99_e2e"]) == 463
+
+
+def test_batch_changes_every_window(orc):
+    # fast (100) / slow (300) instances of the source role under RR, both under batch control (B default 2),
+    # one request per window (j at 1000 j): window j holds request j on instance j mod 2.  Slow windows
+    # violate (300 > 250, Q = 0) -> both instances halve to 1; fast windows are calm (200 <= 250) -> both
+    # reset to 2.  Window 0 (fast, B already 2) changes nothing; windows 1..N-2 change both: 2 (N - 2).
+    N = 50
+    fast = W.cost(h=0, alpha=1, beta=0, tau0=99, gamma=0)
+    slow = W.cost(h=0, alpha=1, beta=0, tau0=299, gamma=0)
+    r = run(orc, srv(2, B=2, inst_cost=[fast, slow], route="rr"), batch_cand(250), [1000 * j for j in range(N)],
+            n_windows=N)
+    s = r["summary"][0]
+    assert int(s["batch_changes"]) == 2 * (N - 2)
+    assert r["records"][0, :, 0].tolist() == [100 if j % 2 == 0 else 300 for j in range(N)]
+    assert [int(r["series"][0, w, i]["B"]) for w in range(4) for i in range(2)] == [2, 2, 2, 2, 1, 1, 2, 2]
+
+
+def test_select_changes_every_window(orc):
+    # one request on LARGE decoding for 1.4e8 ticks: busy(LARGE) = W -> SMALL; busy(SMALL) = 0 -> LARGE; ...
+    # every one of the 140000 window closes before the completion at 1.4e8 switches
+    large = dict(W.cost(h=0, alpha=1, beta=0, tau0=139_999_999, gamma=0), large=1)
+    r = run(orc, srv(2, inst_cost=[large, SMALL], route="select"), sel_cand(10 ** 12), [0])
+    s = r["summary"][0]
+    assert int(s["select_changes"]) == 140000 == int(s["window_closes"])
+    assert r["records"][0, :, 0].tolist() == [140_000_000]
