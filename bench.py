@@ -47,7 +47,8 @@ def workload(args, world):
     seeds = args.seeds * world                          # weak scaling: args.seeds per GPU
     if args.config == 3:
         return W.config3(n_seeds=seeds, n_requests=args.requests)
-    return W.config2(n_seeds=seeds, n_requests=args.requests, series_stride=0)
+    # the per-window mode / queue series of every 4096th replica is written in the timed step
+    return W.config2(n_seeds=seeds, n_requests=args.requests, series_stride=4096, series_windows=512)
 
 
 def workload_name(args):
@@ -186,6 +187,7 @@ def main():
     ap.add_argument("--ref-sample", type=int, default=512)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-flush-leg", action="store_true", help="skip the FLAG_RECORDS metric-flush leg")
     ap.add_argument("--generic", action="store_true", help="A/B only: disable the K1 specialisations")
     ap.add_argument("--mid", action="store_true", help="A/B only: at most the level-1 K1 specialisation")
     args = ap.parse_args()
@@ -218,9 +220,11 @@ def main():
         return g
 
     kflags = (sdas.FLAG_GENERIC if args.generic else 0) | (sdas.FLAG_MID if args.mid else 0)
+    if grid["series_stride"]:
+        kflags |= sdas.FLAG_SERIES
     gv0 = sdas.GridView(pipe, grid_for(0), flags=kflags, rank=rank, world=world)
     L = sdas.results_layout(P, gv0)
-    res = sdas.Result(L, sdas.allocate(L, dev, 0))
+    res = sdas.Result(L, sdas.allocate(L, dev, kflags))
     acc_local = torch.zeros(sdas.NCNT, dtype=torch.int64, device=dev)
     acc_global = torch.zeros(sdas.NCNT, dtype=torch.int64, device=dev)
 
@@ -294,11 +298,15 @@ def main():
     achieved = ALG_WARP_INSTR_PER_DES_EVENT * (loc_des / args.steps) / k1_avg_s / 1e12
     traffic = None
     issue = None
+    try:   # DRAM bytes of one K1 launch of exactly this workload, measured by ncu at bench size
+        dm = json.load(open(os.path.join(ROOT, "profiles", "k1_dram_bench_config%d.json" % args.config)))
+        if dm["replicas"] == reps // args.steps and dm["n_requests"] == args.requests and world == 1:
+            traffic = dm["dram_bytes_per_launch"]
+    except Exception:
+        pass
     try:
         prof = json.load(open(os.path.join(ROOT, "profiles", "k1_ncu_summary.json" if args.config == 2 else
                                            "k1_ncu_summary_config%d.json" % args.config)))
-        if prof.get("dram_bytes_per_des_event") is not None:
-            traffic = prof["dram_bytes_per_des_event"] * (loc_des / args.steps)
         if prof.get("warp_instr_per_des_event") is not None:
             # the same roofline with the ncu-MEASURED instructions per DES event (profiles/): issue utilisation
             w = float(prof["warp_instr_per_des_event"])
@@ -313,7 +321,8 @@ def main():
         # end to end through the public API: host descriptors -> H2D (inside sdas_simulate), the whole
         # sweep + collective, D2H of every result (summaries, cells, best tables) into pinned memory
         pinned = {n: torch.empty(int(getattr(L, n + "_bytes")), dtype=torch.uint8, pin_memory=True)
-                  for n in ("summary", "cell_cnt", "cell_hist", "best_group", "best_row")}
+                  for n in ("summary", "cell_cnt", "cell_hist", "best_group", "best_row") +
+                  (("series",) if kflags & sdas.FLAG_SERIES else ())}
         h2d = 0
         e2e_ms = []
         for k in range(args.steps):
@@ -327,6 +336,7 @@ def main():
             res.t["cell_cnt"].zero_()
             res.t["cell_hist"].zero_()
             r2, table, _, gvk = parallel.sweep(pipe, g, objective="p99_e2e", rank=rank, world=world, device=dev,
+                                                flags=kflags,
                                                 result=res, pipeline=P)
             for n, h in pinned.items():
                 h.copy_(res.t[n][: h.numel()], non_blocking=True)
@@ -340,6 +350,37 @@ def main():
         d2h = sum(h.numel() for h in pinned.values())
         e2e = {"value": msg / (float(t.item()) / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h)}
+
+    flush_leg = None
+    if world == 1 and not args.no_flush_leg:
+        # the metric flush with exact per-request records on (FLAG_RECORDS, SURVEY §8 d.4 "K2"): it is fused
+        # into K1's finalize, so its HBM bytes are averaged over the K1 launch that produces them
+        fflags = kflags | sdas.FLAG_RECORDS
+        gvf = sdas.GridView(pipe, grid_for(500), flags=fflags)
+        Lf = sdas.results_layout(P, gvf)
+        rf = sdas.Result(Lf, sdas.allocate(Lf, dev, fflags))
+        flush.fill_(7)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        sdas.simulate(P, gvf, device=dev, result=rf)
+        b.record(stream)
+        b.synchronize()
+        ms = a.elapsed_time(b)
+        per_rep = args.requests * 8 + sdas.SUMMARY_DTYPE.itemsize
+        nbytes = Lf.n_local_replicas * per_rep
+        gbs = nbytes / (ms / 1e3) / 1e9
+        flush_leg = {"bytes_per_replica": per_rep, "bytes": nbytes, "k1_ms_with_records": ms,
+                     "k1_ms_without_records": statistics.mean(k1_ms), "achieved_gbs": gbs,
+                     "peak_gbs": float(pk.get("hbm_gbs", 7700.0)), "frac": gbs / float(pk.get("hbm_gbs", 7700.0)),
+                     "note": "records (N x 8 B) + summary written by K1's fused finalize; GB/s = those bytes / the "
+                             "K1 launch that writes them (the flush is not a separate phase)"}
+        try:
+            dmr = json.load(open(os.path.join(ROOT, "profiles", "k1_dram_bench_config%d_records.json" % args.config)))
+            if dmr["replicas"] == Lf.n_local_replicas:
+                flush_leg["dram_bytes_measured"] = dmr["dram_bytes_per_launch"]
+        except Exception:
+            pass
+        del rf
 
     if rank == 0:
         line = {
@@ -359,9 +400,10 @@ def main():
                          "note": "K1; achieved = %d algorithmic warp-instr per DES event (SURVEY §8d.4 floor) x "
                                  "DES events / K1 time; peak = %d SMs x 4 issue/clk x %.0f MHz (MEASURED_PEAKS "
                                  "sm_max_mhz)" % (ALG_WARP_INSTR_PER_DES_EVENT, n_sm, f_mhz)},
-            "gpu_launches": 4 * args.steps,
+            "gpu_launches": 4 * args.steps,   # per timed step: K1, K3, K4, K5
             "clocks": clk,
             "e2e": e2e,
+            "metric_flush": flush_leg,
         }
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(args)

@@ -69,6 +69,10 @@ enum { SDAS_SCOPE_REPLICA = 0, SDAS_SCOPE_CELL = 1, SDAS_SCOPE_GROUP = 2, SDAS_S
 #define SDAS_FLAG_GENERIC 16u /* never launch a specialised K1; results are identical
                                  either way -- A/B and parity tests */
 #define SDAS_FLAG_MID 32u     /* at most the level-1 specialisation (A/B and parity tests) */
+#define SDAS_FLAG_CELL_SERIES 128u /* accumulate the cell-summed window series (M15) into buffers.cell_series */
+#define SDAS_FLAG_SPILL 64u   /* force the smallest shared-memory ring size (32 entries) on specialised
+                                 K1 levels, so rings spill to their global extension;
+                                 results are identical either way -- parity tests */
 
 /* implementation limits (DESIGN.md §"Limits") */
 #define SDAS_MAX_ROLES 8
@@ -237,11 +241,18 @@ typedef struct {
   uint32_t k1_variant;       /* K1 specialisation level running this grid: 0 generic,
                                 1 no KV / pacing / classes / LOAD metric / max_ticks / STEPWISE,
                                 2 LEAN (+ single instances, no fan-out) */
-  uint32_t pad;
+  uint32_t ring_s;           /* shared-memory ring size bound; 0xFFFFFFFF = rings whole */
+  uint64_t cell_series_bytes; /* device: SDAS_FLAG_CELL_SERIES buffer (see sdas_buffers.cell_series) */
 } sdas_layout;
 
 typedef struct {
   void *params, *work, *summary, *records, *series, *cell_cnt, *cell_hist, *best_group, *best_row, *trace;
+  void* cell_series;         /* SDAS_FLAG_CELL_SERIES: n_cells x series_windows x n_instances x 8 u64 (zeroed by
+                                the caller; accumulated): per cell, window w < series_windows and instance
+                                {sum integral Q dt, sum busy ticks, replicas that closed window w, sum max Q,
+                                sum max_num_seqs, replicas whose in-link was BATCH, FUNCTION, TOKEN}
+                                (M15 "plus cell-summed series", PAPER.md:231-238 aggregation); every window a
+                                replica closed counts, also before a later overflow (DESIGN.md R-CSER) */
 } sdas_buffers;
 
 /* Sizes of every buffer for (p, grid) on the current device (queries the occupancy). */

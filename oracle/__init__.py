@@ -166,7 +166,7 @@ def lib():
         L.orc_simulate.restype = C.c_int
         L.orc_simulate.argtypes = [C.POINTER(Pipeline), C.POINTER(Grid), C.c_void_p, C.c_uint64, C.c_uint32,
                                    C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p,
-                                   C.c_uint64, C.POINTER(C.c_uint64)]
+                                   C.c_uint64, C.POINTER(C.c_uint64), C.c_void_p]
         L.orc_cells.argtypes = [C.POINTER(Grid), C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         L.orc_argmin_groups.argtypes = [C.POINTER(Grid), C.c_void_p, C.c_uint32, C.c_uint64, C.c_void_p]
         L.orc_pooled_pct.restype = C.c_uint64
@@ -269,8 +269,11 @@ class Problem:
         self.R = self.C * I * K * self.S
 
 
+CELL_SERIES_FIELDS = ["qint", "busy", "n", "maxq", "B", "n_batch", "n_function", "n_token"]
+
+
 def simulate(pipe, grid, ids=None, threads=None, records=True, hists=True, series=False, trace_id=None,
-             trace_cap=1 << 20):
+             trace_cap=1 << 20, cell_series=False):
     """Run the oracle on replica ids (default: the whole grid).  Returns a dict of numpy arrays."""
     p = Problem(pipe, grid)
     if ids is None:
@@ -285,16 +288,20 @@ def simulate(pipe, grid, ids=None, threads=None, records=True, hists=True, serie
     if series and grid["series_stride"]:
         ser = np.zeros((grid["series_slots"], grid["series_windows"], p.n_inst), dtype=SERIES_DTYPE)
     tr = np.zeros(trace_cap, dtype=TRACE_DTYPE) if trace_id is not None else None
+    cser = None
+    if cell_series and grid["series_windows"]:
+        cser = np.zeros((p.I * p.K * p.C, grid["series_windows"], p.n_inst, 8), dtype=np.uint64)
     tn = C.c_uint64(0)
     rc = lib().orc_simulate(C.byref(p.pipe), C.byref(p.grid), ids.ctypes.data, n, threads, summ.ctypes.data,
                             rec.ctypes.data if rec is not None else None,
                             hst.ctypes.data if hst is not None else None,
                             ser.ctypes.data if ser is not None else None,
                             0 if trace_id is None else int(trace_id),
-                            tr.ctypes.data if tr is not None else None, trace_cap, C.byref(tn))
+                            tr.ctypes.data if tr is not None else None, trace_cap, C.byref(tn),
+                            cser.ctypes.data if cser is not None else None)
     if rc != 0:
         raise ValueError("oracle rejected the input (rc=%d)" % rc)
-    out = {"summary": summ, "ids": ids, "records": rec, "hists": hst, "series": ser}
+    out = {"summary": summ, "ids": ids, "records": rec, "hists": hst, "series": ser, "cell_series": cser}
     if tr is not None:
         out["trace"] = tr[: min(tn.value, trace_cap)]
     return out

@@ -30,6 +30,7 @@
 #include <cmath>
 #include <cstring>
 #include <deque>
+#include <mutex>
 #include <queue>
 #include <thread>
 #include <vector>
@@ -267,6 +268,7 @@ struct Replica {
   uint32_t* rec;        // [N][2] or null
   uint32_t* hist;       // [3][NBINS]: e2e, ff, interactive e2e (always provided internally)
   orc_series* series;   // this replica's [windows][n_inst] or null
+  std::vector<uint64_t> cser;   // M15 cell-summed series: this replica's contribution [windows][n_inst][8]
   orc_trace* trace; uint64_t trace_cap; uint64_t* trace_n;
 
   std::vector<Inst> inst;
@@ -579,6 +581,19 @@ struct Replica {
   }
 
   void write_series(uint64_t k) {
+    if (!cser.empty() && k < G.series_windows) {      // M15 cell-summed series (reading R-CSER)
+      for (size_t i = 0; i < inst.size(); ++i) {
+        const Inst& I = inst[i];
+        uint64_t* e = &cser[(k * inst.size() + i) * 8];
+        int32_t il = in_link[I.role];
+        e[0] += I.w_qint;
+        e[1] += I.w_busy;
+        e[2] += 1;                                       // replicas that closed window k
+        e[3] += I.w_maxq;
+        e[4] += I.B;
+        if (il >= 0) e[5 + cur_mode[il]] += 1;           // replicas per in-link mode
+      }
+    }
     if (!series || k >= G.series_windows) return;
     for (size_t i = 0; i < inst.size(); ++i) {
       const Inst& I = inst[i];
@@ -920,13 +935,15 @@ int orc_arrivals(const orc_arrival* a, uint64_t master_seed, uint32_t s_coord, u
 
 int orc_simulate(const orc_pipeline* p, const orc_grid* g, const uint64_t* ids, uint64_t n, uint32_t threads,
                  orc_summary* out, uint32_t* records, uint32_t* hists, orc_series* series, uint64_t trace_id,
-                 orc_trace* trace, uint64_t trace_cap, uint64_t* trace_n) {
+                 orc_trace* trace, uint64_t trace_cap, uint64_t* trace_n, uint64_t* cell_series) {
   if (validate(p, g)) return -1;
   uint32_t n_inst = 0;
   for (uint32_t r = 0; r < p->n_roles; ++r) n_inst += p->roles[r].n_instances;
   if (trace_n) *trace_n = 0;
   std::atomic<uint64_t> next(0);
   std::atomic<int> err(0);
+  std::mutex cs_mu;
+  const uint64_t cs_per_cell = (uint64_t)g->series_windows * n_inst * 8;
   auto worker = [&]() {
     std::vector<uint32_t> hbuf(ORC_NHIST * ORC_NBINS);
     std::vector<uint32_t> rbuf;
@@ -952,7 +969,13 @@ int orc_simulate(const orc_pipeline* p, const orc_grid* g, const uint64_t* ids, 
       R.trace = (trace && rid == trace_id) ? trace : nullptr;
       R.trace_cap = trace_cap;
       R.trace_n = trace_n;
+      if (cell_series && g->series_windows) R.cser.assign(cs_per_cell, 0);
       if (R.run() != 0) err = -1;
+      if (cell_series && g->series_windows) {          // cell (i, k, c) of replica rid
+        const uint64_t cell = (g_idx / g->n_seeds) * g->n_cand + rid % g->n_cand;
+        std::lock_guard<std::mutex> lk(cs_mu);
+        for (uint64_t q = 0; q < cs_per_cell; ++q) cell_series[cell * cs_per_cell + q] += R.cser[q];
+      }
     }
   };
   if (threads < 1) threads = 1;

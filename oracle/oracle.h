@@ -138,11 +138,14 @@ uint32_t orc_mode_step(uint64_t u, uint32_t lo, uint32_t hi, uint64_t window, ui
  * hists:   NULL or [n * ORC_NHIST * ORC_NBINS] u32 (e2e, ff, interactive e2e)
  * series:  NULL or [series_slots * series_windows * n_inst] (indexed by r / stride)
  * trace:   NULL or [trace_cap] for replica trace_id; *trace_n receives the count
+ * cell_series: NULL or [n_cells * series_windows * n_inst * 8] u64, zeroed by the caller: per cell, window
+ *   and instance {sum integral Q, sum busy, replicas that closed the window, sum max Q, sum B, replicas
+ *   whose in-link was BATCH / FUNCTION / TOKEN} over the simulated replicas (M15 cell-summed series)
  * Returns 0 on success, <0 on invalid input. */
 int orc_simulate(const orc_pipeline* p, const orc_grid* g, const uint64_t* ids, uint64_t n,
                  uint32_t threads, orc_summary* out, uint32_t* records, uint32_t* hists,
                  orc_series* series, uint64_t trace_id, orc_trace* trace, uint64_t trace_cap,
-                 uint64_t* trace_n);
+                 uint64_t* trace_n, uint64_t* cell_series);
 
 /* Cell merge over a full grid (cells indexed (i*K + k)*C + c): cnt [n_cells * ORC_NCNT] i64,
  * hist [n_cells * ORC_NHIST * ORC_NBINS] i64.  summaries/hists indexed by global replica id. */

@@ -349,65 +349,97 @@ sdas_status plan(const sdas_pipeline* p, const sdas_grid* g, Plan& pl) {
   for (uint32_t cc = 0; cc < g->n_candidates; ++cc) sel = sel || g->cand[cc].select_role >= 0;
   if (h.lean && !sel && h.n_inst == h.n_roles && h.max_out == 1 && !(g->flags & SDAS_FLAG_MID)) h.lean = 2;
 
-  // --- shared-memory layout of one warp's replica
-  uint64_t o = 256;  // WarpHdr
-  const uint32_t R = p->request_cap;
-  h.off_reqA = (uint32_t)o; o += 8ull * R;
-  h.off_reqFF = (uint32_t)o; o += 8ull * R;              // exact u64 first-feedback latency (M13, M19)
-  h.off_reqJ = (uint32_t)o; o += 4ull * R;
-  h.off_reqO = (uint32_t)o; o += 4ull * R;
-  h.off_reqNit = (uint32_t)o; o += 2ull * R;
-  h.off_reqOut = (uint32_t)o; o += 2ull * R;
-  h.off_reqHome = (uint32_t)o; o += R;                    // u8 KV home per request slot (M21)
-  h.off_reqCls = (uint32_t)o; o += h.cls ? R : 0;         // u8 class per request slot (M26)
-  o = align_up(o, 16);
-  h.off_bitmap = (uint32_t)o; o += 4ull * h.bitmap_words;
-  for (uint32_t i = 0; i < h.n_inst; ++i) {
-    DInst& I = h.inst[i];
+  // --- shared-memory layout of one warp's replica, for a shared-memory ring size bound RS (two-level rings,
+  // a ring of capacity > RS keeps its oldest RS entries in shared memory, the rest in the
+  // warp's extension area of `work`; levels >= 1 only -- level 0 keeps every ring whole)
+  auto layout_for = [&](uint32_t RS) -> uint64_t {
+    uint64_t o = 256;  // WarpHdr
+    const uint32_t R = p->request_cap;
+    h.off_reqA = (uint32_t)o; o += 8ull * R;
+    h.off_reqFF = (uint32_t)o; o += 8ull * R;              // exact u64 first-feedback latency (M13, M19)
+    h.off_reqJ = (uint32_t)o; o += 4ull * R;
+    h.off_reqO = (uint32_t)o; o += 4ull * R;
+    h.off_reqNit = (uint32_t)o; o += 2ull * R;
+    h.off_reqOut = (uint32_t)o; o += 2ull * R;
+    h.off_reqHome = (uint32_t)o; o += R;                    // u8 KV home per request slot (M21)
+    h.off_reqCls = (uint32_t)o; o += h.cls ? R : 0;         // u8 class per request slot (M26)
     o = align_up(o, 16);
-    I.off_inbox = (uint32_t)o; o += 8ull * I.inbox_cap * (h.cls ? 2 : 1);   // class-1 ring follows (M27)
-    if (h.kv_role && I.role == h.kv_role) o += 4ull * I.inbox_cap;  // hinted-transfer ready ticks (M23)
+    h.off_bitmap = (uint32_t)o; o += 4ull * h.bitmap_words;
+    uint64_t gx = 0;
+    for (uint32_t i = 0; i < h.n_inst; ++i) {
+      DInst& I = h.inst[i];
+      const uint64_t pin = std::min(I.inbox_cap, RS), pfl = std::min(I.flight_cap, RS), pwt = std::min(I.wait_cap, RS);
+      o = align_up(o, 16);
+      I.off_inbox = (uint32_t)o; o += 8ull * pin * (h.cls ? 2 : 1);   // class-1 ring follows (M27)
+      if (h.kv_role && I.role == h.kv_role) o += 4ull * pin;         // hinted-transfer ready ticks (M23)
+      o = align_up(o, 16);
+      I.off_ftick = (uint32_t)o; o += 4ull * pfl;
+      o = align_up(o, 16);
+      I.off_fbody = (uint32_t)o; o += 8ull * pfl;
+      if (h.kv_role && I.role == h.kv_role) o += 4ull * pfl;         // hinted-transfer ready ticks (M23)
+      o = align_up(o, 16);
+      I.off_wait = (uint32_t)o; o += 4ull * pwt * (h.cls ? 2 : 1);
+      o = align_up(o, 16);
+      I.off_batch = (uint32_t)o; o += 4ull * 32 * h.role[I.role].batch_words;
+      I.gx_inbox = (uint32_t)gx; gx = align_up(gx + 8ull * (I.inbox_cap - pin), 16);
+      I.gx_ftick = (uint32_t)gx; gx = align_up(gx + 4ull * (I.flight_cap - pfl), 16);
+      I.gx_fbody = (uint32_t)gx; gx = align_up(gx + 8ull * (I.flight_cap - pfl), 16);
+      I.gx_wait = (uint32_t)gx; gx = align_up(gx + 4ull * (I.wait_cap - pwt), 16);
+    }
+    h.gx_per_warp = align_up(gx, 256);
     o = align_up(o, 16);
-    I.off_ftick = (uint32_t)o; o += 4ull * I.flight_cap;
-    o = align_up(o, 16);
-    I.off_fbody = (uint32_t)o; o += 8ull * I.flight_cap;
-    if (h.kv_role && I.role == h.kv_role) o += 4ull * I.flight_cap;    // hinted-transfer ready ticks (M23)
-    o = align_up(o, 16);
-    I.off_wait = (uint32_t)o; o += 4ull * I.wait_cap * (h.cls ? 2 : 1);
-    o = align_up(o, 16);
-    I.off_batch = (uint32_t)o; o += 4ull * 32 * h.role[I.role].batch_words;
-  }
-  o = align_up(o, 16);
-  h.off_scratch = 256;
-  const uint64_t need = std::max<uint64_t>(o, 256 + (uint64_t)kScratchMin);
-  h.smem_per_warp = (uint32_t)align_up(need, 16);
+    h.off_scratch = 256;
+    return align_up(std::max<uint64_t>(o, 256 + (uint64_t)kScratchMin), 16);
+  };
   h.off_warps = (uint32_t)align_up(sizeof(DParams), 128);
-
-  // --- occupancy: choose warps per block maximizing resident warps per SM
   const uint64_t smem_cap = 227 * 1024;
-  if (h.off_warps + h.smem_per_warp > smem_cap)
+  int n_sm = 148;
+  // occupancy: warps per block maximizing resident warps per SM for a given per-warp footprint
+  auto occupancy = [&](uint64_t per_warp, uint32_t rs, uint32_t& bw, uint32_t& bb) -> uint64_t {
+    uint64_t best_tot = 0;
+    bw = 1; bb = 0;
+    for (uint32_t wpb = 1; wpb <= 8; ++wpb) {
+      const uint64_t sb = h.off_warps + (uint64_t)wpb * per_warp;
+      if (sb > smem_cap) break;
+      int bps = 0, nsm = 0;
+      if (query_occupancy(wpb, (uint32_t)sb, h.max_out, h.cls, h.lean, rs != 0xFFFFFFFFu, &bps, &nsm) == 0) {
+        n_sm = nsm;
+        if (bps <= 0) continue;                 // block exceeds the instantiation's launch bound
+      } else {
+        bps = (int)std::min<uint64_t>(32, (228 * 1024) / (sb + 1024));
+        bps = std::min(bps, (int)(64 / wpb));
+      }
+      const uint64_t tot = (uint64_t)bps * wpb;
+      if (tot >= best_tot) { best_tot = tot; bw = wpb; bb = (uint32_t)bps; }
+    }
+    return best_tot;
+  };
+  // ring size bound: the largest of (whole rings, 512, 256, ..., 32) that reaches the most resident warps
+  // (level 0 and FLAG_SPILL = one choice each)
+  uint32_t max_cap = 0;
+  for (uint32_t i = 0; i < h.n_inst; ++i)
+    max_cap = std::max(max_cap, std::max(h.inst[i].inbox_cap, std::max(h.inst[i].flight_cap, h.inst[i].wait_cap)));
+  std::vector<uint32_t> cand_rs;
+  if (!h.lean) cand_rs = {0xFFFFFFFFu};
+  else if (g->flags & SDAS_FLAG_SPILL) cand_rs = {32u};
+  else {
+    cand_rs = {0xFFFFFFFFu};
+    for (uint32_t rs = 512; rs >= 32; rs /= 2)
+      if (rs < max_cap) cand_rs.push_back(rs);
+  }
+  uint32_t best_rs = cand_rs[0], best_w = 1, best_b = 0;
+  uint64_t best_tot = 0;
+  for (uint32_t rs : cand_rs) {
+    const uint64_t per = layout_for(rs);
+    uint32_t bw = 1, bb = 0;
+    const uint64_t tot = per + h.off_warps <= smem_cap ? occupancy(per, rs, bw, bb) : 0;
+    if (tot > best_tot) { best_tot = tot; best_rs = rs; best_w = bw; best_b = bb; }
+  }
+  h.ring_s = best_rs;
+  h.smem_per_warp = (uint32_t)layout_for(best_rs);
+  if (best_tot == 0 || h.off_warps + h.smem_per_warp > smem_cap)
     return fail(SDAS_E_LIMIT, "replica needs %u B of shared memory (max %llu): reduce caps or request_cap",
                 h.smem_per_warp, (unsigned long long)(smem_cap - h.off_warps));
-  int n_sm = 148;
-  uint32_t best_w = 1, best_b = 1;
-  uint64_t best_tot = 0;
-  bool have_dev = false;
-  for (uint32_t wpb = 1; wpb <= 8; ++wpb) {
-    const uint64_t sb = h.off_warps + (uint64_t)wpb * h.smem_per_warp;
-    if (sb > smem_cap) break;
-    int bps = 0, nsm = 0;
-    if (query_occupancy(wpb, (uint32_t)sb, h.max_out, h.cls, h.lean, &bps, &nsm) == 0) {
-      have_dev = true;
-      n_sm = nsm;
-      if (bps <= 0) continue;                 // block exceeds the instantiation's launch bound
-    } else {
-      bps = (int)std::min<uint64_t>(32, (228 * 1024) / (sb + 1024));
-      bps = std::min(bps, (int)(64 / wpb));
-    }
-    const uint64_t tot = (uint64_t)bps * wpb;
-    if (tot >= best_tot) { best_tot = tot; best_w = wpb; best_b = (uint32_t)bps; }
-  }
-  (void)have_dev;
   pl.wpb = best_w;
   pl.blocks_per_sm = best_b;
   pl.n_sm = (uint32_t)n_sm;
@@ -416,6 +448,7 @@ sdas_status plan(const sdas_pipeline* p, const sdas_grid* g, Plan& pl) {
   pl.blocks = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)n_sm * best_b, want_blocks));
   pl.total_warps = (uint64_t)pl.blocks * best_w;
   h.off_rec_cls = sizeof(Work) + pl.total_warps * (uint64_t)g->n_requests * 8ull;
+  h.off_gx = align_up(sizeof(Work) + pl.total_warps * (uint64_t)g->n_requests * 9ull, 256);
 
   // --- blob: DParams | candidates | arrivals | LIST ticks
   uint64_t b = align_up(sizeof(DParams), 64);
@@ -474,7 +507,9 @@ sdas_status fill_layout(const Plan& pl, const sdas_grid* g, sdas_layout* L) {
   const DParams& h = pl.hp;
   L->params_bytes = pl.blob_bytes;
   const uint64_t scratch = pl.total_warps * (uint64_t)g->n_requests * 9ull;   // records + class bytes
-  L->work_bytes = align_up(sizeof(Work) + std::max<uint64_t>(scratch, pl.n_cells * 4ull), 256);
+  L->work_bytes = align_up(std::max<uint64_t>(h.off_gx + pl.total_warps * h.gx_per_warp,
+                                              sizeof(Work) + pl.n_cells * 4ull), 256);
+  (void)scratch;
   L->summary_bytes = align_up(std::max<uint64_t>(1, h.n_local_replicas) * SDAS_SUMMARY_BYTES, 256);
   L->records_bytes = (g->flags & SDAS_FLAG_RECORDS) ? align_up(h.n_local_replicas * g->n_requests * 8ull, 256) : 0;
   L->series_bytes = (g->flags & SDAS_FLAG_SERIES)
@@ -496,6 +531,9 @@ sdas_status fill_layout(const Plan& pl, const sdas_grid* g, sdas_layout* L) {
   L->blocks_per_sm = pl.blocks_per_sm;
   L->resident_replicas = pl.total_warps;
   L->k1_variant = h.lean;
+  L->ring_s = h.ring_s;
+  L->cell_series_bytes = (g->flags & SDAS_FLAG_CELL_SERIES)
+                             ? align_up(pl.n_cells * (uint64_t)g->series_windows * h.n_inst * 64ull, 256) : 0;
   return SDAS_OK;
 }
 
@@ -606,6 +644,8 @@ static sdas_status run_sim(const sdas_pipeline* p, const sdas_grid* g, const sda
   if ((g->flags & SDAS_FLAG_RECORDS) && !d->records) return fail(SDAS_E_BUFFER, "FLAG_RECORDS needs records");
   if ((g->flags & SDAS_FLAG_SERIES) && !d->series) return fail(SDAS_E_BUFFER, "FLAG_SERIES needs series");
   if ((g->flags & SDAS_FLAG_TRACE) && !d->trace) return fail(SDAS_E_BUFFER, "FLAG_TRACE needs trace");
+  if ((g->flags & SDAS_FLAG_CELL_SERIES) && g->series_windows && !d->cell_series)
+    return fail(SDAS_E_BUFFER, "FLAG_CELL_SERIES needs cell_series");
   std::vector<uint8_t> blob;
   pack_blob(g, pl, blob);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);

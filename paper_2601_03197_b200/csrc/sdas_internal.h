@@ -13,10 +13,13 @@ constexpr unsigned long long kUnsetFF = ~0ull;   // first-feedback latency not y
 constexpr uint32_t kNever = 0xFFFFFFFFu;
 constexpr int kScratchMin = SDAS_NHIST * SDAS_NBINS * 4 + 256 * 4 + SDAS_SUMMARY_BYTES + SDAS_NCNT * 8;  // finalize scratch
 
-struct DInst {          // one instance, 64 B
+struct DInst {          // one instance, 80 B
   uint32_t role, h, alpha, beta, tau0, gamma, B_default, flags;   // flags: bit0 large, bit1 svc_exp
-  uint32_t inbox_cap, flight_cap, wait_cap;
+  uint32_t inbox_cap, flight_cap, wait_cap;                       // logical capacities (M14)
   uint32_t off_inbox, off_ftick, off_fbody, off_wait, off_batch;  // byte offsets inside the warp region
+  // two-level rings: a ring whose capacity exceeds DParams.ring_s keeps its oldest ring_s
+  // entries in shared memory and the rest in this warp's extension area of `work` (byte offsets below)
+  uint32_t gx_inbox, gx_ftick, gx_fbody, gx_wait;
 };
 
 struct DRole {          // one role, 64 B
@@ -65,6 +68,8 @@ struct alignas(16) DParams {
   uint32_t max_out, need_lint, kv_role, kv_ctx, kv_tau, off_reqHome;
   uint32_t cls, off_reqCls;   // f2: two request classes (class-1 rings follow the class-0 rings)
   uint32_t need_pace, lean;   // f4: some link or candidate paces (M30); lean: K1 specialisation (§5.3)
+  uint32_t ring_s, pad_rs;    // shared-memory ring size bound (levels >= 1; 0xFFFFFFFF = every ring whole)
+  uint64_t off_gx, gx_per_warp;   // ring extension areas in `work`: warp w's at off_gx + w * gx_per_warp
   uint64_t off_rec_cls;       // f2: byte offset in `work` of the per-warp record-class arrays
   uint64_t kv_skew32;         // M21: home = instance 0 iff ATTR.w2 < kv_skew32 = floor(skew * 2^32 / 1000)
   uint64_t window, slo, max_ticks, master_seed;
@@ -75,7 +80,7 @@ struct alignas(16) DParams {
   DLink link[SDAS_MAX_LINKS + 1];
 };
 
-static_assert(sizeof(DInst) == 64, "DInst");
+static_assert(sizeof(DInst) == 80, "DInst");
 static_assert(sizeof(DRole) == 64, "DRole");
 static_assert(sizeof(DCand) == 80, "DCand");
 static_assert(sizeof(DArr) == 80, "DArr");
@@ -94,7 +99,8 @@ int launch_group_argmin(const uint8_t* params_dev, const DParams& hp, const sdas
                         uint64_t slo, void* stream);
 int launch_finalize(const uint8_t* params_dev, const DParams& hp, const sdas_buffers* b, uint32_t objective,
                     uint64_t slo, uint64_t n_cells, uint64_t n_rows, void* stream);
-int query_occupancy(uint32_t warps_per_block, uint32_t smem_bytes, uint32_t maxout, uint32_t cls, uint32_t lean, int* blocks_per_sm,
+int query_occupancy(uint32_t warps_per_block, uint32_t smem_bytes, uint32_t maxout, uint32_t cls, uint32_t lean,
+                    uint32_t spill, int* blocks_per_sm,
                     int* n_sm);
 const char* cuda_error_string(int code);
 

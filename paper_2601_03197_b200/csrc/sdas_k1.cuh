@@ -28,13 +28,13 @@
 #define K1_LEAN_THREADS K1_LB_THREADS
 #define K1_LEAN_MAXREG K1_LB_MAXREG
 #endif
-template <bool TRACE, int MAXOUT, bool CLS, int LV>
+template <bool TRACE, int MAXOUT, bool CLS, int LV, bool SPL>
 __global__ void __launch_bounds__(LV == 2 ? K1_LEAN_THREADS : K1_LB_THREADS)
 __maxnreg__(LV == 2 ? K1_LEAN_MAXREG : K1_LB_MAXREG)
 k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* __restrict__ summary,
             unsigned long long* __restrict__ records_out, uint8_t* __restrict__ series,
             long long* __restrict__ cell_cnt, int* __restrict__ cell_hist, uint8_t* __restrict__ trace_buf,
-            const __grid_constant__ DParams Pk) {   // scalars from parameter space (uniform registers)
+            unsigned long long* __restrict__ cell_series, const __grid_constant__ DParams Pk) {   // scalars from parameter space (uniform registers)
   extern __shared__ __align__(16) uint8_t smem[];
   {
     const uint4* src = reinterpret_cast<const uint4*>(blob);
@@ -76,7 +76,17 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
   const bool is_inst = lane < (int)n_inst;
   const DInst& MI = P.inst[is_inst ? lane : 0];
   const uint32_t my_role = LEAN ? (uint32_t)lane : MI.role;
-  const uint32_t my_inbox_cap = MI.inbox_cap, my_flight_cap = MI.flight_cap, my_wait_cap = MI.wait_cap;
+  // two-level rings (levels >= 1): a ring keeps its oldest RS entries in shared memory and
+  // the rest in this warp's extension area of `work`; the my_*_cap registers hold the shared-memory sizes
+  // min(capacity, RS) and the logical capacities (overflow, rule M14) are read from MI only past them
+  constexpr bool SPILL = SPL;                          // a separate instantiation: grids whose rings fit whole
+  static_assert(!SPL || LV >= 1, "two-level rings exist on the specialised levels only");   // never pay for it
+  const uint32_t RS = SPILL ? Pk.ring_s : 0xFFFFFFFFu;
+  const uint32_t my_inbox_cap = min(MI.inbox_cap, RS), my_flight_cap = min(MI.flight_cap, RS),
+                 my_wait_cap = min(MI.wait_cap, RS);
+  auto gxa = [&](uint32_t off) -> uint8_t* {           // extension area of this warp (cold paths only)
+    return reinterpret_cast<uint8_t*>(work) + Pk.off_gx + gwarp * Pk.gx_per_warp + off;
+  };
   uint8_t* const my_inbox = Wr + MI.off_inbox;
   uint8_t* const my_ftick = Wr + MI.off_ftick;
   uint8_t* const my_fbody = Wr + MI.off_fbody;
@@ -120,7 +130,17 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
     int32_t qlm = -(1 << 30), q_last_sel = -(1 << 30);   // lane l: last change of link l's mode
     uint32_t rr_l = 0;                                    // lane r: round-robin counter of role r
     uint32_t sel_l = lane < (int)Pk.n_roles ? P.role[lane].large_inst : 0u;  // lane r: SELECT target
-    if (lane == 0) *H = WarpHdr{};
+    if (lane == 0) {
+      *H = WarpHdr{};
+      uint32_t ss = 0xFFFFFFFFu;                          // series slot, computed once per replica (M15)
+      if ((Pk.flags & SDAS_FLAG_SERIES) && Pk.series_stride) {
+        const unsigned long long rid = g * C + c;
+        if (rid % Pk.series_stride == 0 && rid / Pk.series_stride < Pk.series_slots)
+          ss = (uint32_t)(rid / Pk.series_stride);
+      }
+      H->ser_slot = ss;
+      H->cell = (uint32_t)(((g / Pk.S) % (Pk.I * (unsigned long long)Pk.K)) * C + c);
+    }
     for (uint32_t w = lane; w < Pk.bitmap_words; w += 32) {
       const uint32_t rem = R_cap - w * 32;
       bitmap[w] = rem >= 32 ? 0xFFFFFFFFu : ((1u << rem) - 1u);
@@ -279,7 +299,8 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
         ovf = true;
         return;
       }
-      const uint32_t idx = wrap_add(__shfl_sync(FULL, fh, dest), fn_d, D.flight_cap);
+      const uint32_t pm_d = min(D.flight_cap, RS);
+      const uint32_t idx = wrap_add(__shfl_sync(FULL, fh, dest), fn_d, pm_d);
       uint32_t tick = t_lo + net;
       if (need_pace) {                     // M30: dispatch at max(t, previous dispatch + gap)
         const uint32_t gp = pace_gap(l);
@@ -294,10 +315,16 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
         }
       }
       if (lane == 0) {
-        at<uint32_t>(Wr, D.off_ftick)[idx] = tick;
-        at<unsigned long long>(Wr, D.off_fbody)[idx] = make_body(slot, flags, tokens, n_in);
-        if (kv_role && P.link[l].dst == kv_role)          // M23 HINT: the transfer starts at routing
-          at<uint32_t>(Wr, D.off_fbody + 8u * D.flight_cap)[idx] = t_lo + Pk.kv_tau * Pk.kv_ctx;
+        if (!SPILL || fn_d < pm_d) {
+          at<uint32_t>(Wr, D.off_ftick)[idx] = tick;
+          at<unsigned long long>(Wr, D.off_fbody)[idx] = make_body(slot, flags, tokens, n_in);
+          if (kv_role && P.link[l].dst == kv_role)          // M23 HINT: the transfer starts at routing
+            at<uint32_t>(Wr, D.off_fbody + 8u * D.flight_cap)[idx] = t_lo + Pk.kv_tau * Pk.kv_ctx;
+        } else {                                            // past the shared-memory part: extension
+          const uint32_t gi = wrap_add(H->gh[1][dest], fn_d - RS, D.flight_cap - RS);
+          reinterpret_cast<uint32_t*>(gxa(D.gx_ftick))[gi] = tick;
+          reinterpret_cast<unsigned long long*>(gxa(D.gx_fbody))[gi] = make_body(slot, flags, tokens, n_in);
+        }
       }
       if (lane == (int)dest) {
         if (fn == 0) fhead = tick;
@@ -385,9 +412,13 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
           if (lane == 0) at<uint32_t>(Wr, I.off_wait)[I.wait_cap + idx] = slot | (out << 16);
           if (lane == (int)i) ++wn1;
         } else {
-          const uint32_t idx = wrap_add(__shfl_sync(FULL, wh, i), wn_i - (CLS ? __shfl_sync(FULL, wn1, i) : 0u),
-                                        I.wait_cap);
-          if (lane == 0) at<uint32_t>(Wr, I.off_wait)[idx] = slot | (out << 16);
+          const uint32_t pmw = min(I.wait_cap, RS), k = wn_i - (CLS ? __shfl_sync(FULL, wn1, i) : 0u);
+          const uint32_t idx = wrap_add(__shfl_sync(FULL, wh, i), k, pmw);
+          if (lane == 0) {
+            if (!SPILL || k < pmw) at<uint32_t>(Wr, I.off_wait)[idx] = slot | (out << 16);
+            else reinterpret_cast<uint32_t*>(gxa(I.gx_wait))[wrap_add(H->gh[2][i], k - RS, I.wait_cap - RS)] =
+                     slot | (out << 16);
+          }
         }
         if (lane == (int)i) ++wn;
         if (TRACE) trace(TR_ITEM_WAIT, i, rJ[slot], out);
@@ -507,10 +538,16 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
               }
               const uint32_t tick = __shfl_sync(FULL, my_tick, __ffs(grp) - 1);   // group's first message
               if ((grp >> lane) & 1u) {
-                const uint32_t pos = __popc(grp & lanemask_lt());
-                const uint32_t idx = wrap_add(fh_d, fn_d + pos, D.flight_cap);
-                at<uint32_t>(Wr, D.off_ftick)[idx] = my_tick;
-                at<unsigned long long>(Wr, D.off_fbody)[idx] = make_body(slot, flags, tokens, n_in);
+                const uint32_t k = fn_d + __popc(grp & lanemask_lt()), pm_d = min(D.flight_cap, RS);
+                if (!SPILL || k < pm_d) {
+                  const uint32_t idx = wrap_add(fh_d, k, pm_d);
+                  at<uint32_t>(Wr, D.off_ftick)[idx] = my_tick;
+                  at<unsigned long long>(Wr, D.off_fbody)[idx] = make_body(slot, flags, tokens, n_in);
+                } else {                                     // past the shared-memory part: extension
+                  const uint32_t gi = wrap_add(H->gh[1][dk], k - RS, D.flight_cap - RS);
+                  reinterpret_cast<uint32_t*>(gxa(D.gx_ftick))[gi] = my_tick;
+                  reinterpret_cast<unsigned long long*>(gxa(D.gx_fbody))[gi] = make_body(slot, flags, tokens, n_in);
+                }
                 if (flags & 1u) atomicAdd(&rO[slot], 1u);          // M13: +1 per opening message
                 if (TRACE) trace_lane(TR_EMIT, dk, rJ[slot], tokens | ((flags & 1u) << 16) | (((flags >> 1) & 1u) << 17) | (l << 20));
               }
@@ -627,7 +664,14 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
           ih1 = wrap_add(ih1, 1u, my_inbox_cap);
           --in1;
         } else {
+          const uint32_t oih = ih;
           ih = wrap_add(ih, 1u, my_inbox_cap);
+          if (SPILL && in > my_inbox_cap) {   // refill the vacated slot with the oldest extension entry
+            const uint32_t g0 = H->gh[0][lane];
+            reinterpret_cast<unsigned long long*>(my_inbox)[oih] =
+                reinterpret_cast<const unsigned long long*>(gxa(MI.gx_inbox))[g0];
+            H->gh[0][lane] = (uint16_t)wrap_add(g0, 1u, MI.inbox_cap - RS);
+          }
         }
         --in;
       }
@@ -655,7 +699,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
           const uint32_t k = lane - bi;
           const uint32_t* const wr = at<uint32_t>(Wr, I.off_wait);
           const uint32_t e = (CLS && k < n1) ? wr[I.wait_cap + wrap_add(wh1_i, k, I.wait_cap)]
-                                             : wr[wrap_add(wh_i, k - n1, I.wait_cap)];
+                                             : wr[wrap_add(wh_i, k - n1, min(I.wait_cap, RS))];
           const uint32_t out = e >> 16;
           wA = (e & 0xFFFu) | (out << 16);
           for (uint32_t q = 0; q < n_out; ++q) {
@@ -674,6 +718,15 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
           if (MAXOUT > 1) { bat[96 + lane] = wD; bat[128 + lane] = 0xFF00u; }
         }
         __syncwarp();
+        const uint32_t pmw = min(I.wait_cap, RS);
+        if (SPILL && wn_i > pmw) {   // refill the vacated slots with the oldest extension entries
+          const uint32_t m = min(nadm, wn_i - pmw), g0 = H->gh[2][i], cx = I.wait_cap - RS;
+          if (lane < (int)m)
+            at<uint32_t>(Wr, I.off_wait)[wrap_add(wh_i, lane, pmw)] =
+                reinterpret_cast<const uint32_t*>(gxa(I.gx_wait))[wrap_add(g0, lane, cx)];
+          __syncwarp();
+          if (lane == 0) H->gh[2][i] = (uint16_t)wrap_add(g0, m, cx);
+        }
       }
       const uint32_t nbat = bi + nadm;
       // branch-free update of instance i (tau0 < 2^31 and gamma*32 < 2^30 are validated: no u32 overflow)
@@ -775,7 +828,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
         }
         const uint32_t dest = route(0, slot);
         if (TRACE) trace(TR_ARRIVE, j, 1, dest);
-        const bool bad = lane == (int)dest && in >= my_inbox_cap;
+        const bool bad = lane == (int)dest && in >= my_inbox_cap && (!SPILL || in >= MI.inbox_cap);
         if (lane == (int)dest && !bad) {
           unsigned long long* const ib = reinterpret_cast<unsigned long long*>(my_inbox);
           const unsigned long long body = make_body(slot, F_OPENS | F_CLOSES, P_next, P_next);
@@ -783,7 +836,10 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
             ib[my_inbox_cap + wrap_add(ih1, in1, my_inbox_cap)] = body;
             ++in1;
           } else {
-            ib[wrap_add(ih, in - (CLS ? in1 : 0u), my_inbox_cap)] = body;
+            const uint32_t k = in - (CLS ? in1 : 0u);
+            if (!SPILL || k < my_inbox_cap) ib[wrap_add(ih, k, my_inbox_cap)] = body;
+            else reinterpret_cast<unsigned long long*>(gxa(MI.gx_inbox))[wrap_add(H->gh[0][lane], k - RS,
+                                                                                 MI.inbox_cap - RS)] = body;
           }
           ++in;
           if (coalesce) cut_run();
@@ -898,14 +954,9 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
       }
     };
     auto close_window = [&](bool final_partial) {
-      SeriesRec* ser = nullptr;
-      if ((Pk.flags & SDAS_FLAG_SERIES) && Pk.series_stride) {
-        const unsigned long long rid = (Pk.first_group + (x / C) * Pk.world) * C + c;
-        if (rid % Pk.series_stride == 0 && rid / Pk.series_stride < Pk.series_slots)
-          ser = reinterpret_cast<SeriesRec*>(series) +
-                (rid / Pk.series_stride) * (unsigned long long)Pk.series_windows * n_inst;
-      }
-      if (ser && wk < Pk.series_windows && is_inst) {
+      const uint32_t ss = H->ser_slot;
+      if (ss != 0xFFFFFFFFu && wk < Pk.series_windows && is_inst) {
+        SeriesRec* const ser = reinterpret_cast<SeriesRec*>(series) + (unsigned long long)ss * Pk.series_windows * n_inst;
         const int32_t il = P.role[my_role].in_link;
         SeriesRec r;
         r.qint = acc_qint;
@@ -914,6 +965,17 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
         r.mode = il < 0 ? 255 : (uint8_t)((modes >> (2 * il)) & 3u);
         r.B = (uint8_t)Bk;
         ser[(unsigned long long)wk * n_inst + lane] = r;
+      }
+      if ((Pk.flags & SDAS_FLAG_CELL_SERIES) && wk < Pk.series_windows && is_inst) {   // M15 cell-summed series
+        unsigned long long* const e =
+            cell_series + (((unsigned long long)H->cell * Pk.series_windows + wk) * n_inst + lane) * 8u;
+        const int32_t il = P.role[my_role].in_link;
+        atomicAdd(e + 0, acc_qint);
+        atomicAdd(e + 1, (unsigned long long)acc_busy);
+        atomicAdd(e + 2, 1ull);
+        atomicAdd(e + 3, (unsigned long long)acc_maxq);
+        atomicAdd(e + 4, (unsigned long long)Bk);
+        if (il >= 0) atomicAdd(e + 5 + ((modes >> (2 * il)) & 3u), 1ull);
       }
       if (!final_partial) {
         if (lane == 0) ++H->window_closes;
@@ -977,22 +1039,35 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
         bool lovf = false;
         if (dv) {
           if (coalesce) cut_run();
-          const uint32_t* ft = reinterpret_cast<const uint32_t*>(my_ftick);
-          const unsigned long long* fb = reinterpret_cast<const unsigned long long*>(my_fbody);
+          uint32_t* const ft = reinterpret_cast<uint32_t*>(my_ftick);
+          unsigned long long* const fb = reinterpret_cast<unsigned long long*>(my_fbody);
           unsigned long long* ib = reinterpret_cast<unsigned long long*>(my_inbox);
           for (;;) {
-            if (K1_UNLIKELY(in >= my_inbox_cap)) { lovf = true; break; }
+            if (K1_UNLIKELY(in >= my_inbox_cap) && (!SPILL || in >= MI.inbox_cap)) { lovf = true; break; }
             const unsigned long long body = fb[fh];
             if (CLS && prio && rCls[body & 0xFFFFu]) {        // M27: class-1 ring
               ib[my_inbox_cap + wrap_add(ih1, in1, my_inbox_cap)] = body;
               ++in1;
             } else {
-              const uint32_t at_idx = wrap_add(ih, in - (CLS ? in1 : 0u), my_inbox_cap);
-              ib[at_idx] = body;
-              if (my_kv) my_iready[at_idx] = my_fready[fh];        // emission + tau*ctx (M23 HINT)
+              const uint32_t k = in - (CLS ? in1 : 0u);
+              if (!SPILL || k < my_inbox_cap) {
+                const uint32_t at_idx = wrap_add(ih, k, my_inbox_cap);
+                ib[at_idx] = body;
+                if (my_kv) my_iready[at_idx] = my_fready[fh];        // emission + tau*ctx (M23 HINT)
+              } else {
+                reinterpret_cast<unsigned long long*>(gxa(MI.gx_inbox))[wrap_add(H->gh[0][lane], k - RS,
+                                                                                 MI.inbox_cap - RS)] = body;
+              }
             }
             ++in;
+            const uint32_t ofh = fh;
             fh = wrap_add(fh, 1u, my_flight_cap);
+            if (SPILL && fn > my_flight_cap) {   // refill the vacated slot with the oldest extension entry
+              const uint32_t g0 = H->gh[1][lane];
+              ft[ofh] = reinterpret_cast<const uint32_t*>(gxa(MI.gx_ftick))[g0];
+              fb[ofh] = reinterpret_cast<const unsigned long long*>(gxa(MI.gx_fbody))[g0];
+              H->gh[1][lane] = (uint16_t)wrap_add(g0, 1u, MI.flight_cap - RS);
+            }
             --fn;
             ++cnt_deliv;
             if (TRACE) trace_lane(TR_DELIVER, lane, rJ[body & 0xFFFFu], (uint32_t)(body >> 32) & 0xFFFFu);
@@ -1054,7 +1129,6 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
 
     // ---------------------------------------------------------------- finalize (M18, M19)
     uint8_t* const sum_out = summary + x * SDAS_SUMMARY_BYTES;
-    const unsigned long long rid = g * C + c;
     const unsigned long long cell = ((g / Pk.S) % (Pk.I * (unsigned long long)Pk.K)) * C + c;
     uint32_t* const stg = scratch + SDAS_NHIST * SDAS_NBINS + 256;   // 44 summary words, then counters
     unsigned long long* const cst = reinterpret_cast<unsigned long long*>(stg + SDAS_SUMMARY_BYTES / 4);

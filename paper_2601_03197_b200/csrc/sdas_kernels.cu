@@ -41,8 +41,10 @@ struct WarpHdr {                        // per-replica counters owned by lane 0 
   uint32_t n_sat, good, w_n, w_good;
   uint32_t w_half, window_closes, mode_switches, batch_changes;
   uint32_t select_changes, completed_int, rejected, good_int;   // f2 (M28, M29)
-  uint32_t gate_changes, pad0, pad1, pad2;
+  uint32_t gate_changes, ser_slot, cell, pad2;   // ser_slot: this replica's series slot, 0xFFFFFFFF = none;
+                                                 // cell: (i*K + k)*C + c
   unsigned long long pace_free[8];               // f4 M30: per link, earliest tick of the next dispatch
+  uint16_t gh[3][8];   // two-level rings: head of the inbox / in-flight / wait extension per instance
 };
 static_assert(sizeof(WarpHdr) <= 256, "WarpHdr");
 
@@ -302,23 +304,28 @@ __global__ void k5_row_argmin(const uint8_t* __restrict__ blob, const long long*
 
 // ------------------------------------------------------------------------------ launchers
 typedef void (*K1Fn)(const uint8_t*, Work*, uint8_t*, unsigned long long*, uint8_t*, long long*, int*, uint8_t*,
-                     DParams);
+                     unsigned long long*, DParams);
 
-static K1Fn k1_pick(bool trace, uint32_t maxout, bool cls, uint32_t lv) {
-  if (!trace && !cls && lv == 2 && maxout == 1) return k1_simulate<false, 1, false, 2>;
-  if (!trace && !cls && lv >= 1) return maxout > 1 ? k1_simulate<false, 2, false, 1> : k1_simulate<false, 1, false, 1>;
-  if (cls) {
-    if (maxout > 1) return trace ? k1_simulate<true, 2, true, 0> : k1_simulate<false, 2, true, 0>;
-    return trace ? k1_simulate<true, 1, true, 0> : k1_simulate<false, 1, true, 0>;
+static K1Fn k1_pick(bool trace, uint32_t maxout, bool cls, uint32_t lv, bool spill) {
+  if (!trace && !cls && lv == 2 && maxout == 1)
+    return spill ? k1_simulate<false, 1, false, 2, true> : k1_simulate<false, 1, false, 2, false>;
+  if (!trace && !cls && lv >= 1) {
+    if (maxout > 1) return spill ? k1_simulate<false, 2, false, 1, true> : k1_simulate<false, 2, false, 1, false>;
+    return spill ? k1_simulate<false, 1, false, 1, true> : k1_simulate<false, 1, false, 1, false>;
   }
-  if (maxout > 1) return trace ? k1_simulate<true, 2, false, 0> : k1_simulate<false, 2, false, 0>;
-  return trace ? k1_simulate<true, 1, false, 0> : k1_simulate<false, 1, false, 0>;
+  if (cls) {
+    if (maxout > 1) return trace ? k1_simulate<true, 2, true, 0, false> : k1_simulate<false, 2, true, 0, false>;
+    return trace ? k1_simulate<true, 1, true, 0, false> : k1_simulate<false, 1, true, 0, false>;
+  }
+  if (maxout > 1) return trace ? k1_simulate<true, 2, false, 0, false> : k1_simulate<false, 2, false, 0, false>;
+  return trace ? k1_simulate<true, 1, false, 0, false> : k1_simulate<false, 1, false, 0, false>;
 }
 
 int launch_simulate(const uint8_t* params_dev, const DParams& hp, const sdas_buffers* bf, uint32_t blocks,
                     uint32_t warps_per_block, uint32_t smem_bytes, void* stream, const uint64_t* log2_table) {
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  const K1Fn fn = k1_pick((hp.flags & SDAS_FLAG_TRACE) != 0, hp.max_out, hp.cls != 0, hp.lean);
+  const K1Fn fn = k1_pick((hp.flags & SDAS_FLAG_TRACE) != 0, hp.max_out, hp.cls != 0, hp.lean,
+                          hp.ring_s != 0xFFFFFFFFu);
   cudaError_t e = cudaMemcpyToSymbolAsync(c_log2, log2_table, sizeof(uint64_t) * 257, 0, cudaMemcpyHostToDevice, s);
   if (e != cudaSuccess) return (int)e;
   e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes);
@@ -338,7 +345,7 @@ int launch_simulate(const uint8_t* params_dev, const DParams& hp, const sdas_buf
       params_dev, reinterpret_cast<Work*>(bf->work), reinterpret_cast<uint8_t*>(bf->summary),
       reinterpret_cast<unsigned long long*>(bf->records), reinterpret_cast<uint8_t*>(bf->series),
       reinterpret_cast<long long*>(bf->cell_cnt), reinterpret_cast<int*>(bf->cell_hist),
-      reinterpret_cast<uint8_t*>(bf->trace), hp);
+      reinterpret_cast<uint8_t*>(bf->trace), reinterpret_cast<unsigned long long*>(bf->cell_series), hp);
   return (int)cudaGetLastError();
 }
 
@@ -374,10 +381,11 @@ int launch_finalize(const uint8_t* params_dev, const DParams& hp, const sdas_buf
 }
 
 int query_occupancy(uint32_t warps_per_block, uint32_t smem_bytes, uint32_t maxout, uint32_t cls, uint32_t lean,
+                    uint32_t spill,
                     int* blocks_per_sm, int* n_sm) {
   {  // a block larger than the instantiation's launch bound cannot launch
     cudaFuncAttributes fa;
-    const cudaError_t ea = cudaFuncGetAttributes(&fa, k1_pick(false, maxout, cls != 0, lean));
+    const cudaError_t ea = cudaFuncGetAttributes(&fa, k1_pick(false, maxout, cls != 0, lean, spill != 0));
     if (ea != cudaSuccess) return (int)ea;
     if ((int)(warps_per_block * 32) > fa.maxThreadsPerBlock) {
       *blocks_per_sm = 0;
@@ -392,7 +400,7 @@ int query_occupancy(uint32_t warps_per_block, uint32_t smem_bytes, uint32_t maxo
   if (e != cudaSuccess) return (int)e;
   e = cudaDeviceGetAttribute(n_sm, cudaDevAttrMultiProcessorCount, dev);
   if (e != cudaSuccess) return (int)e;
-  const K1Fn fn = k1_pick(false, maxout, cls != 0, lean);
+  const K1Fn fn = k1_pick(false, maxout, cls != 0, lean, spill != 0);
   e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes);
   if (e != cudaSuccess) return (int)e;
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, fn, (int)warps_per_block * 32, smem_bytes);

@@ -44,6 +44,9 @@ def reduce_cells(result, group=None):
     hist = result.t["cell_hist"][: L.n_cells * sdas.NHIST * sdas.NBINS * 4].view(dtype=torch.int32)
     _all_reduce_sum(cnt, group)
     _all_reduce_sum(hist, group)
+    cs = result.t.get("cell_series")
+    if cs is not None and cs.numel():                  # M15 cell-summed series: integer sums as well
+        _all_reduce_sum(cs[: L.cell_series_bytes].view(dtype=torch.int64), group)
 
 
 def gather_best_groups(result, n_groups, rank, world, group=None):

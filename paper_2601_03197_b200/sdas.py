@@ -35,7 +35,9 @@ OBJECTIVES = {"p99_e2e": 0, "p50_e2e": 1, "p99_ff": 2, "throughput": 3, "goodput
 INTENTS = {None: 0, "max_throughput": 1, "min_p90_latency": 2}
 CONSTRAINT_METRICS = {"e2e_p90": 0, "e2e_p99": 1}
 SCOPES = {"replica": 0, "cell": 1, "group": 2, "row": 3}
-FLAG_RECORDS, FLAG_SERIES, FLAG_TRACE, FLAG_STEPWISE, FLAG_GENERIC, FLAG_MID = 1, 2, 4, 8, 16, 32
+FLAG_RECORDS, FLAG_SERIES, FLAG_TRACE, FLAG_STEPWISE, FLAG_GENERIC, FLAG_MID, FLAG_SPILL = 1, 2, 4, 8, 16, 32, 64
+FLAG_CELL_SERIES = 128
+CELL_SERIES_FIELDS = ["qint", "busy", "n", "maxq", "B", "n_batch", "n_function", "n_token"]
 NBINS, NCNT, NHIST = 464, 28, 3
 ROUTE_NONE = 255
 
@@ -133,11 +135,11 @@ class Layout(C.Structure):
         "n_local_groups", "n_groups", "n_cells", "n_rows", "n_replicas")] + [
         ("n_instances", C.c_uint32), ("smem_per_replica", C.c_uint32), ("warps_per_block", C.c_uint32),
         ("blocks_per_sm", C.c_uint32), ("resident_replicas", C.c_uint64), ("k1_variant", C.c_uint32),
-        ("pad", C.c_uint32)]
+        ("ring_s", C.c_uint32), ("cell_series_bytes", C.c_uint64)]
 
 
 BUFFER_NAMES = ["params", "work", "summary", "records", "series", "cell_cnt", "cell_hist", "best_group",
-                "best_row", "trace"]
+                "best_row", "trace", "cell_series"]
 
 
 class Buffers(C.Structure):
@@ -408,6 +410,12 @@ class Result:
         hist = self.t["cell_hist"][: nc * NHIST * NBINS * 4].cpu().numpy().view(np.int32).reshape(nc, NHIST, NBINS)
         return cnt, hist
 
+    def cell_series(self, windows, n_inst):
+        """M15 cell-summed series: (n_cells, windows, n_inst, 8) u64, fields CELL_SERIES_FIELDS."""
+        nc = self.layout.n_cells
+        return self.t["cell_series"][: nc * windows * n_inst * 64].cpu().numpy().view(np.uint64).reshape(
+            nc, windows, n_inst, 8)
+
     def best_group(self):
         return self.t["best_group"][: self.layout.n_local_groups * 4].cpu().numpy().view(np.int32)
 
@@ -428,16 +436,19 @@ def _needs(layout, flags):
             "series": layout.series_bytes if flags & FLAG_SERIES else 0,
             "cell_cnt": layout.cell_cnt_bytes, "cell_hist": layout.cell_hist_bytes,
             "best_group": layout.best_group_bytes, "best_row": layout.best_row_bytes,
-            "trace": layout.trace_bytes if flags & FLAG_TRACE else 0}
+            "trace": layout.trace_bytes if flags & FLAG_TRACE else 0,
+            "cell_series": layout.cell_series_bytes if flags & FLAG_CELL_SERIES else 0}
 
 
 def allocate(layout, device, flags):
     import torch
     need = _needs(layout, flags)
     t = {k: torch.empty(int(v), dtype=torch.uint8, device=device) for k, v in need.items()
-         if v and k not in ("cell_cnt", "cell_hist")}
+         if v and k not in ("cell_cnt", "cell_hist", "cell_series")}
     t["cell_cnt"] = torch.zeros(int(layout.cell_cnt_bytes), dtype=torch.uint8, device=device)
     t["cell_hist"] = torch.zeros(int(layout.cell_hist_bytes), dtype=torch.uint8, device=device)
+    if flags & FLAG_CELL_SERIES and layout.cell_series_bytes:
+        t["cell_series"] = torch.zeros(int(layout.cell_series_bytes), dtype=torch.uint8, device=device)
     return t
 
 

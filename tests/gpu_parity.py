@@ -14,10 +14,11 @@ BINS = ["bin_p50_e2e", "bin_p99_e2e", "bin_p50_ff", "bin_p99_ff"]
 
 
 def run_gpu(pipe, grid, records=True, series=False, trace_replica=None, objective=None, objective_slo=0,
-            rank=0, world=1, group_range=None, stepwise=False, generic=False, mid=False):
+            rank=0, world=1, group_range=None, stepwise=False, generic=False, mid=False, spill=False):
     flags = (sdas.FLAG_RECORDS if records else 0) | (sdas.FLAG_SERIES if series else 0)
     flags |= (sdas.FLAG_STEPWISE if stepwise else 0) | (sdas.FLAG_GENERIC if generic else 0)
     flags |= sdas.FLAG_MID if mid else 0
+    flags |= sdas.FLAG_SPILL if spill else 0
     P = sdas.Pipeline(pipe)
     gv = sdas.GridView(pipe, grid, flags=flags, rank=rank, world=world, group_range=group_range,
                        trace_replica=trace_replica, trace_cap=1 << 18)
@@ -79,9 +80,9 @@ def first_divergence(a, b):
     return None
 
 
-def full_check(pipe, grid, series=False, objective="p99_e2e", objective_slo=0, threads=None):
+def full_check(pipe, grid, series=False, objective="p99_e2e", objective_slo=0, threads=None, **kw):
     """GPU vs oracle on a whole (small) grid: summaries, records, series, cells, argmins."""
-    g = run_gpu(pipe, grid, records=True, series=series, objective=objective, objective_slo=objective_slo)
+    g = run_gpu(pipe, grid, records=True, series=series, objective=objective, objective_slo=objective_slo, **kw)
     o = oracle.simulate(pipe, grid, series=series, threads=threads)
     compare_summaries(g["summary"], o["summary"])
     compare_records(g["records"], o["records"], g["summary"])

@@ -24,4 +24,4 @@ for r in range(reps):
         sdas.simulate(P, gv, result=res)
         e1.record()
         torch.cuda.synchronize()
-        print(cfg, name, res.layout.k1_variant, round(e0.elapsed_time(e1), 1), flush=True)
+        print(cfg, name, res.layout.k1_variant, res.layout.ring_s, round(e0.elapsed_time(e1), 1), flush=True)
