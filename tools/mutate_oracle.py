@@ -100,6 +100,9 @@ MUTANTS = [
     ("rows: pooled percentile rank floor(q n)", "M18 pooled rows",
      [("const uint64_t k = (num * n + 99) / 100;\n  uint64_t cum = 0;", "const uint64_t k = (num * n) / 100 + 1;\n  uint64_t cum = 0;")],
      [T_ARG + "::test_pooled_percentile_brute_force"]),
+    ("cell series: integral of the JSQ load instead of Q", "M15 / R-CSER",
+     [("e[0] += I.w_qint;", "e[0] += I.w_lint;")],
+     ["tests/test_oracle_cellseries.py::test_ht9_cell_series_hand_values"]),
     ("rows: bad = any overflow (truncated ignored)", "M20 / R-KEYS",
      [("k.bad = q[1] != q[0];", "k.bad = q[2] != 0;")],
      [T_ARG + "::test_row_argmin_brute_force_random"]),
