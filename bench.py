@@ -39,19 +39,32 @@ def env_rank():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
 
 
-DEFAULT_SEEDS = {2: 2048, 3: 4096}                       # 1,048,576 replicas per GPU either way
+DEFAULT_SEEDS = {2: 2048, 3: 4096, 4: 1, 5: 2}           # 1,048,576 replicas per GPU in every config
+OBJECTIVE = {4: ("large_under_slo", 6_000_000)}           # config 4 ranks by the large fraction under the SLO
 
 
 def workload(args, world):
-    """(pipeline, grid) of the timed workload: BASELINE config 2 (default) or config 3, weak-scaled."""
+    """(pipeline, grid) of the timed workload: BASELINE config 2 (default) or 3, or the full config 4 / 5 grid
+    (every candidate x rate x profile) with fewer seeds: 1 (config 4) / 2 (config 5) per GPU = 1M replicas."""
     seeds = args.seeds * world                          # weak scaling: args.seeds per GPU
     if args.config == 3:
         return W.config3(n_seeds=seeds, n_requests=args.requests)
+    if args.config == 4:
+        return W.config4(n_seeds=seeds, n_requests=args.requests)
+    if args.config == 5:
+        return W.config5(n_seeds=seeds, n_requests=args.requests)
     # the per-window mode / queue series of every 4096th replica (SURVEY §8 d.3) is written in the timed step
     return W.config2(n_seeds=seeds, n_requests=args.requests, series_stride=4096, series_windows=512)
 
 
 def workload_name(args):
+    if args.config == 4:
+        return ("config4 grid at %d seed(s)/GPU: P2-MS dev{LARGE,SMALL}->tester, MMPP-2 bursts, model selection, "
+                "16384 policies x 16 mean rates x 4 burst ratios, N=%d requests/replica (objective large_under_slo, "
+                "6 s); the full 16M-replica config is 16 seeds" % (args.seeds, args.requests))
+    if args.config == 5:
+        return ("config5 grid at %d seeds/GPU: P2-X, 4096 strategies (3 static + 4093 adaptive policies) x 128 "
+                "rates, N=%d requests/replica; the full 64M-replica config is 128 seeds" % (args.seeds, args.requests))
     if args.config == 3:
         return ("config3: P4-chain planner->coder(2)->tester(2)->reviewer, 16 candidates (modes x RR/JSQ routing x "
                 "SLO batch control) x 16 Poisson rates x %d seeds/GPU, N=%d requests/replica" % (args.seeds,
@@ -180,8 +193,9 @@ def main():
     ap.add_argument("--steps", type=int, default=2)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="sdas", choices=["sdas", "reference"])
-    ap.add_argument("--config", type=int, default=2, choices=[2, 3],
-                    help="BASELINE config timed: 2 (default, the headline) or 3 (4-agent routed DAG)")
+    ap.add_argument("--config", type=int, default=2, choices=[2, 3, 4, 5],
+                    help="BASELINE config timed: 2 (default, the headline), 3 (4-agent routed DAG), or a 1M-replica "
+                         "per GPU slice of 4 (MMPP + model selection) / 5 (full strategy sweep)")
     ap.add_argument("--seeds", type=int, default=None, help="seeds per GPU (default: 1M replicas per GPU)")
     ap.add_argument("--requests", type=int, default=1000)
     ap.add_argument("--ref-sample", type=int, default=512)
@@ -222,6 +236,7 @@ def main():
     kflags = (sdas.FLAG_GENERIC if args.generic else 0) | (sdas.FLAG_MID if args.mid else 0)
     if grid["series_stride"]:
         kflags |= sdas.FLAG_SERIES
+    obj, obj_slo = OBJECTIVE.get(args.config, ("p99_e2e", 0))
     gv0 = sdas.GridView(pipe, grid_for(0), flags=kflags, rank=rank, world=world)
     L = sdas.results_layout(P, gv0)
     res = sdas.Result(L, sdas.allocate(L, dev, kflags))
@@ -236,7 +251,7 @@ def main():
         ev[0].record(stream)
         sdas.simulate(P, gv, device=dev, result=res)                   # K1
         ev[1].record(stream)
-        sdas.group_argmin(P, gv, res, objective="p99_e2e", device=dev)  # K3
+        sdas.group_argmin(P, gv, res, objective=obj, objective_slo=obj_slo, device=dev)  # K3
         ev[2].record(stream)
         cnt_view = res.t["cell_cnt"][: L.n_cells * sdas.NCNT * 8].view(torch.int64).view(L.n_cells, sdas.NCNT)
         if timed:
@@ -246,7 +261,7 @@ def main():
             parallel.reduce_cells(res)
             parallel.gather_best_groups(res, L.n_groups, rank, world)
         ev[4].record(stream)
-        sdas.finalize(P, gv, res, objective="p99_e2e", device=dev)     # K4 + K5
+        sdas.finalize(P, gv, res, objective=obj, objective_slo=obj_slo, device=dev)     # K4 + K5
         ev[5].record(stream)
         if timed:
             acc_global.add_(cnt_view.sum(0))
@@ -335,8 +350,8 @@ def main():
             a.record(stream)
             res.t["cell_cnt"].zero_()
             res.t["cell_hist"].zero_()
-            r2, table, _, gvk = parallel.sweep(pipe, g, objective="p99_e2e", rank=rank, world=world, device=dev,
-                                                flags=kflags,
+            r2, table, _, gvk = parallel.sweep(pipe, g, objective=obj, objective_slo=obj_slo, rank=rank, world=world,
+                                                device=dev, flags=kflags,
                                                 result=res, pipeline=P)
             for n, h in pinned.items():
                 h.copy_(res.t[n][: h.numel()], non_blocking=True)

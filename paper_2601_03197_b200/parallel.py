@@ -49,11 +49,13 @@ def reduce_cells(result, group=None):
         _all_reduce_sum(cs[: L.cell_series_bytes].view(dtype=torch.int64), group)
 
 
-def gather_best_groups(result, n_groups, rank, world, group=None):
-    """all_gather of the per-group best tables -> global int32 table [n_groups] on every rank."""
+def gather_best_groups(result, n_groups, rank, world, group=None, group_range=None):
+    """all_gather of the per-group best tables -> global int32 table [n_groups] on every rank (-1 outside
+    group_range)."""
     import torch
     import torch.distributed as dist
-    per = (n_groups + world - 1) // world
+    gb, ge = group_range if group_range is not None else (0, n_groups)
+    per = (ge - gb + world - 1) // world + 1
     L = result.layout
     mine = torch.full((per,), -1, dtype=torch.int32, device=result.t["best_group"].device)
     n = L.n_local_groups
@@ -65,23 +67,23 @@ def gather_best_groups(result, n_groups, rank, world, group=None):
     out = [torch.empty_like(mine) for _ in range(world)]
     dist.all_gather(out, mine, group=group)
     out = [o.to(dev) for o in out]
-    table = torch.empty(n_groups, dtype=torch.int32, device=dev)
+    table = torch.full((n_groups,), -1, dtype=torch.int32, device=dev)
     for r in range(world):
-        ids = torch.as_tensor(local_group_ids(n_groups, r, world), device=dev)
+        ids = torch.as_tensor(local_group_ids(n_groups, r, world, group_range), device=dev)
         table[ids] = out[r][: len(ids)]
     return table
 
 
 def sweep(pipe, grid, objective="p99_e2e", objective_slo=0, rank=0, world=1, device="cuda", group=None,
-          flags=0, result=None, pipeline=None):
+          flags=0, result=None, pipeline=None, group_range=None):
     """One full distributed sweep: K1 + K3 on the local partition, the collective, then K4/K5.
     Returns (result, global best-group table or None, pipeline, grid view)."""
     P = pipeline or sdas.Pipeline(pipe)
-    gv = sdas.GridView(pipe, grid, flags=flags, rank=rank, world=world)
+    gv = sdas.GridView(pipe, grid, flags=flags, rank=rank, world=world, group_range=group_range)
     res = sdas.control_sweep(P, gv, objective=objective, objective_slo=objective_slo, device=device, result=result)
     table = None
     if world > 1:
         reduce_cells(res, group)
-        table = gather_best_groups(res, res.layout.n_groups, rank, world, group)
+        table = gather_best_groups(res, res.layout.n_groups, rank, world, group, group_range)
     sdas.finalize(P, gv, res, objective=objective, objective_slo=objective_slo, device=device)
     return res, table, P, gv

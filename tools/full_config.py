@@ -15,6 +15,7 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 import workloads as W  # noqa: E402
+from bench import ClockSampler  # noqa: E402
 from paper_2601_03197_b200 import sdas  # noqa: E402
 
 cfg = sys.argv[1]
@@ -28,12 +29,15 @@ L = sdas.results_layout(P, gv)
 res = sdas.Result(L, sdas.allocate(L, torch.device("cuda", 0), 0))
 e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
 torch.cuda.synchronize()
+clocks = ClockSampler(0)                                  # nvidia-smi clocks / throttle reasons during the run
+clocks.start()
 e[0].record()
 sdas.control_sweep(P, gv, objective=objective, objective_slo=slo, result=res)
 e[1].record()
 sdas.finalize(P, gv, res, objective=objective, objective_slo=slo)
 e[2].record()
 torch.cuda.synchronize()
+clk = clocks.stop()
 k1k3_ms, fin_ms = e[0].elapsed_time(e[1]), e[1].elapsed_time(e[2])
 cnt, _ = res.cells()
 F = {n: i for i, n in enumerate(sdas.CELL_FIELDS)}
@@ -43,7 +47,8 @@ des = msg + int(tot[F["recv_steps"]] + tot[F["decode_steps"]] + tot[F["window_cl
 out = {"workload": "%s full: %d replicas x %d requests, 1 GPU, objective %s" % (cfg, R, grid["n_requests"], objective),
        "k1_k3_ms": k1k3_ms, "k4_k5_ms": fin_ms, "replicas": int(tot[F["n_replicas"]]),
        "msg_events_per_s": msg / ((k1k3_ms + fin_ms) / 1e3), "des_events_per_s": des / ((k1k3_ms + fin_ms) / 1e3),
-       "replicas_per_s": R / ((k1k3_ms + fin_ms) / 1e3), "k1_variant": L.k1_variant}
+       "replicas_per_s": R / ((k1k3_ms + fin_ms) / 1e3), "k1_variant": L.k1_variant, "ring_s": L.ring_s,
+       "warps_per_sm": L.warps_per_block * L.blocks_per_sm, "clocks": clk}
 if n_sample:
     import oracle
     from gpu_parity import compare_summaries
