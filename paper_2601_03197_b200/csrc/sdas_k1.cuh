@@ -79,6 +79,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
   // two-level rings (levels >= 1): a ring keeps its oldest RS entries in shared memory and
   // the rest in this warp's extension area of `work`; the my_*_cap registers hold the shared-memory sizes
   // min(capacity, RS) and the logical capacities (overflow, rule M14) are read from MI only past them
+  constexpr bool LAZY = LV == 2;   // deliveries into a busy instance are not events
   constexpr bool SPILL = SPL;                          // a separate instantiation: grids whose rings fit whole
   static_assert(!SPL || LV >= 1, "two-level rings exist on the specialised levels only");   // never pay for it
   const uint32_t RS = SPILL ? Pk.ring_s : 0xFFFFFFFFu;
@@ -438,6 +439,19 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
       item_done(slot);
     };
 
+    // lane-local: a message due at tick x will enter this instance's inbox while it may be mid-run: end the
+    // run at the first step boundary >= x (the cut of M7's RECV-first START, applied when x becomes known)
+    auto cut_at = [&](uint32_t x) {
+      if (st != DECODE || runm <= 1u) return;
+      const uint32_t c = max(1u, MI.tau0 + MI.gamma * b);
+      const uint32_t rs = end_lo - runm * c;
+      const uint32_t mp = (x - rs + c - 1u) / c;
+      if (mp < runm) {
+        runm = mp;
+        end_lo = rs + mp * c;
+      }
+    };
+
     // ---------------------------------------------------------------- phase COMPLETE: DECODE (M7, M9, M13)
     auto complete_decode = [&](uint32_t i) {
       const DInst& I = P.inst[i];
@@ -554,6 +568,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
               if (lane == (int)dk) {
                 if (fn == 0) fhead = tick;
                 fn += cnt;
+                if (LAZY) cut_at(tick);                    // the delivery will not be an event of its own
               }
             }
             __syncwarp();
@@ -677,6 +692,77 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
       }
       if (TRACE) trace(TR_RECV_START, i, rJ[__shfl_sync(FULL, slot, i)], __shfl_sync(FULL, cost32, i));
     };
+    // AHEAD: emit now the messages of the emission points the source instance i passes at
+    // steps 1 .. m-1 of its run (step k's messages carry emission tick t + k c, in batch order, M9); the
+    // net delay is below one step, so at each emission tick the destination's in-flight ring holds exactly
+    // that step's messages (M14); a step whose messages do not fit next to the ring's current content ends
+    // the run there (its messages are then emitted by complete_decode, with the exact overflow test).
+    // Returns the (possibly shorter) run length.  Lanes < nbat hold the batch words wA, wB.
+    auto emit_ahead = [&](uint32_t i, const DRole& R, uint32_t nbat, uint32_t cost32, uint32_t m, uint32_t wA,
+                          uint32_t wB) -> uint32_t {
+      const uint32_t l = R.out_link0, dk = P.link[l].dst;   // LEAN: role = instance
+      const DInst& D = P.inst[dk];
+      uint32_t* const bat = at<uint32_t>(Wr, P.inst[i].off_batch);
+      const bool act = lane < (int)nbat;
+      const uint32_t out = wA >> 16, mode = (wA >> 12) & 3u, slot = wA & 0xFFFu;
+      const uint32_t done0 = wB & 0xFFFFu;
+      uint32_t nxt = wB >> 16;
+      uint32_t wC = act ? bat[64 + lane] : 0u;
+      uint32_t prev = wC & 0xFFFFu, fidx = (wC >> 16) & 0xFFu;
+      const uint32_t chunk = P.link[l].chunk, Fp = min(R.n_functions, out), net = P.link[l].net;
+      uint32_t fn_d = __shfl_sync(FULL, fn, dk);
+      const uint32_t fh_d = __shfl_sync(FULL, fh, dk), pm_d = min(D.flight_cap, RS);
+      bool moved = false;
+      for (;;) {
+        const uint32_t s = (act && nxt < out) ? nxt - done0 : 0xFFFFFFFFu;   // step of the next emission
+        const uint32_t k = __reduce_min_sync(FULL, s);
+        if (k >= m) break;                                 // at the run end or beyond: complete_decode
+        const uint32_t em = __ballot_sync(FULL, s == k);
+        const uint32_t cnt = __popc(em);
+        if (fn_d + cnt > D.flight_cap) { m = k; break; }   // no room next to the ring's content: end here
+        const uint32_t tick = t_lo + k * cost32 + net;
+        if (s == k) {
+          const bool tm = mode == SDAS_TOKEN;
+          const uint32_t tokens = nxt - prev;
+          const uint32_t flags = (tm ? (prev == 0 ? 1u : 0u) : 1u) | ((tm ? (nxt == out ? 1u : 0u) : 1u) << 1);
+          const uint32_t n_in = tm ? out : tokens;
+          const uint32_t q = fn_d + __popc(em & lanemask_lt());
+          const unsigned long long body = make_body(slot, flags, tokens, n_in);
+          if (!SPILL || q < pm_d) {
+            const uint32_t idx = wrap_add(fh_d, q, pm_d);
+            at<uint32_t>(Wr, D.off_ftick)[idx] = tick;
+            at<unsigned long long>(Wr, D.off_fbody)[idx] = body;
+          } else {
+            const uint32_t gi = wrap_add(H->gh[1][dk], q - RS, D.flight_cap - RS);
+            reinterpret_cast<uint32_t*>(gxa(D.gx_ftick))[gi] = tick;
+            reinterpret_cast<unsigned long long*>(gxa(D.gx_fbody))[gi] = body;
+          }
+          if (flags & 1u) atomicAdd(&rO[slot], 1u);       // M13: +1 per opening message
+          prev = nxt;
+          if (mode == SDAS_FUNCTION) {
+            ++fidx;
+            nxt = min((uint32_t)(((unsigned long long)(fidx + 1u) * out) / Fp), 0xFFFFu);
+          } else {                                          // TOKEN (BATCH emits at the end only)
+            nxt = min(nxt + chunk, out);
+          }
+        }
+        if (lane == (int)dk) {
+          if (fn == 0) fhead = tick;
+          fn += cnt;
+          cut_at(tick);
+        }
+        fn_d += cnt;
+        moved = true;
+      }
+      if (moved) {
+        if (act) {
+          bat[32 + lane] = done0 | (nxt << 16);
+          bat[64 + lane] = prev | (fidx << 16) | (dk << 24);
+        }
+        __syncwarp();
+      }
+      return m;
+    };
     auto start_decode = [&](uint32_t i) {  // FIFO admission (modes bound here, M9) + DECODE step / run
       const DInst& I = P.inst[i];
       const uint32_t role = LEAN ? i : I.role;
@@ -732,7 +818,12 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
       // branch-free update of instance i (tau0 < 2^31 and gamma*32 < 2^30 are validated: no u32 overflow)
       const bool me = lane == (int)i;
       const uint32_t cost32 = max(1u, I.tau0 + I.gamma * nbat);
-      // run length: steps until the first sequence reaches an emission point / its end / first feedback
+      // run length: steps until the first sequence reaches an emission point / its end / first feedback.
+      // AHEAD: the source role's inbox receives arrivals only, so its run is known up to the
+      // next arrival; its emission points do not end the run -- their messages are emitted now, each with
+      // its own emission tick, and the run ends at a finish / first feedback / arrival / window bound
+      const bool ahead = LAZY && role == 0 && n_out == 1 && nbat > 0 && P.link[R.out_link0].net < cost32 &&
+                         nbat <= P.inst[P.link[R.out_link0].dst].flight_cap;
       uint32_t m = 1;
       if (coalesce) {
         uint32_t sk = 0xFFFFFFFFu;
@@ -744,7 +835,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
         if (lane < (int)nbat) {
           const uint32_t done = wB & 0xFFFFu;
           uint32_t lim = wA >> 16;                                      // out
-          if (n_out > 0) lim = min(lim, wB >> 16);
+          if (n_out > 0 && !ahead) lim = min(lim, wB >> 16);
           if (MAXOUT > 1 && n_out > 1) lim = min(lim, wD & 0xFFFFu);
           sk = (role == ((modes >> 28) & 7u) && done == 0u) ? 1u : lim - done;
         }
@@ -753,6 +844,10 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
           // keep every pending tick < 2^31 ahead; end at the first boundary >= the next window when the
           // controller could change B while items wait; never step past max_ticks
           if ((unsigned long long)m * cost32 >= (1ull << 30)) m = max(1u, (1u << 30) / cost32);
+          if (LAZY) {                                      // end at the first boundary >= a pending delivery
+            const uint32_t fn_i = __shfl_sync(FULL, fn, i), fh_i = __shfl_sync(FULL, fhead, i);
+            if (fn_i) m = min(m, max(1u, (fh_i - t_lo + cost32 - 1u) / cost32));
+          }
           const uint32_t span = m * cost32;
           if ((modes >> 31) && wn_i > nadm) {
             const uint32_t nbd = nb_lo - t_lo;
@@ -760,7 +855,9 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
           }
           if (max_ticks && t + span > max_ticks)
             m = (uint32_t)max(1ull, (max_ticks - min(t, max_ticks)) / cost32);
+          if (ahead && arr_near) m = min(m, max(1u, (A_lo - t_lo + cost32 - 1u) / cost32));   // next arrival
         }
+        if (ahead && m > 1) m = emit_ahead(i, R, nbat, cost32, m, wA, wB);
       }
       wh = me ? wrap_add(wh, nadm - n1, my_wait_cap) : wh;
       wn = me ? wn - nadm : wn;
@@ -988,14 +1085,68 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
       if (lane == 0) { H->w_n = 0; H->w_good = 0; H->w_half = 0; }
     };
 
+    // lane-local DELIVER: move the in-flight head messages due by now (strict: due before now) into the
+    // inbox; returns true on an inbox overflow (M14).  LAZY moves of messages due before now add the inbox
+    // time they missed to the window integral and their step to max Q (the state after DELIVER at their
+    // tick, which was not an event); messages due now enter the next integration step as in the model.
+    auto deliver = [&](bool strict) -> bool {
+      uint32_t* const ft = reinterpret_cast<uint32_t*>(my_ftick);
+      unsigned long long* const fb = reinterpret_cast<unsigned long long*>(my_fbody);
+      unsigned long long* ib = reinterpret_cast<unsigned long long*>(my_inbox);
+      for (;;) {
+        if (K1_UNLIKELY(in >= my_inbox_cap) && (!SPILL || in >= MI.inbox_cap)) return true;
+        const unsigned long long body = fb[fh];
+        if (CLS && prio && rCls[body & 0xFFFFu]) {        // M27: class-1 ring
+          ib[my_inbox_cap + wrap_add(ih1, in1, my_inbox_cap)] = body;
+          ++in1;
+        } else {
+          const uint32_t k = in - (CLS ? in1 : 0u);
+          if (!SPILL || k < my_inbox_cap) {
+            const uint32_t at_idx = wrap_add(ih, k, my_inbox_cap);
+            ib[at_idx] = body;
+            if (my_kv) my_iready[at_idx] = my_fready[fh];        // emission + tau*ctx (M23 HINT)
+          } else {
+            reinterpret_cast<unsigned long long*>(gxa(MI.gx_inbox))[wrap_add(H->gh[0][lane], k - RS,
+                                                                             MI.inbox_cap - RS)] = body;
+          }
+        }
+        ++in;
+        if (LAZY && fhead != t_lo) {                       // due before now (window split: see close)
+          acc_qint += t_lo - fhead;
+          acc_maxq = max(acc_maxq, in + wn);
+        }
+        const uint32_t ofh = fh;
+        fh = wrap_add(fh, 1u, my_flight_cap);
+        if (SPILL && fn > my_flight_cap) {   // refill the vacated slot with the oldest extension entry
+          const uint32_t g0 = H->gh[1][lane];
+          ft[ofh] = reinterpret_cast<const uint32_t*>(gxa(MI.gx_ftick))[g0];
+          fb[ofh] = reinterpret_cast<const unsigned long long*>(gxa(MI.gx_fbody))[g0];
+          H->gh[1][lane] = (uint16_t)wrap_add(g0, 1u, MI.flight_cap - RS);
+        }
+        --fn;
+        ++cnt_deliv;
+        if (TRACE) trace_lane(TR_DELIVER, lane, rJ[body & 0xFFFFu], (uint32_t)(body >> 32) & 0xFFFFu);
+        if (fn == 0) return false;
+        fhead = ft[fh];
+        if (LAZY ? (int32_t)(fhead - t_lo) > (strict ? -1 : 0) : fhead != t_lo) return false;
+      }
+    };
+
     // ---------------------------------------------------------------- event loop (M12)
+#ifdef K1_COUNT_ITERS
+    uint32_t n_iter = 0;   // experiment builds only (tools/iters.py): event-loop iterations -> summary word 42
+#endif
     for (;;) {
+#ifdef K1_COUNT_ITERS
+      ++n_iter;
+#endif
       __syncwarp();
       if (!arr_more && nsys == 0) break;   // (arr_more == jn < N, kept in a register)
       // next tick: warp-min over 32-bit deltas (every pending event lies < 2^31 ticks ahead)
       // (branch-free: lanes that are not instances hold IDLE / empty state and contribute nothing)
       uint32_t d = st != IDLE ? end_lo - t_lo : 0xFFFFFFFFu;
-      d = fn ? min(d, fhead - t_lo) : d;
+      // LAZY: only idle instances (and any whose inbox could fill) wait for their deliveries as events
+      d = fn && (!LAZY || st == IDLE || in + fn > my_inbox_cap) ? min(d, fhead - t_lo) : d;
       const uint32_t d0 = min(nb_lo - t_lo, arr_near ? A_lo - t_lo : 0xFFFFFFFFu);
       d = lane == 0 ? min(d, d0) : d;
       d = __reduce_min_sync(FULL, d);
@@ -1010,6 +1161,9 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
       int_nsys += (unsigned long long)nsys * d;
       t += d;
       t_lo += d;
+      // LAZY: messages delivered since the last event to a busy instance enter its inbox now -- before the
+      // window split, and before COMPLETE's emissions test the in-flight rings (M14 counts undelivered only)
+      if (LAZY && fn && (int32_t)(fhead - t_lo) < 0) deliver(true);
       if (K1_UNLIKELY(t_lo == nb_lo)) {  // phase 0 WINDOW
         close_window(false);
         nb_lo += W32;
@@ -1031,50 +1185,17 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
         } while (cm);
         if (K1_UNLIKELY(ovf)) break;
       }
-      // phase 2 DELIVER (per destination instance, FIFO; lane = instance)
-      const bool dv = fn > 0 && fhead == t_lo;
+      // phase 2 DELIVER (per destination instance, FIFO; lane = instance).  LAZY: a busy destination's
+      // deliveries are not events of their own; they are moved here at its next event, with
+      // the inbox time they missed added to the window integral
+      const bool dv = fn > 0 && (LAZY ? (int32_t)(fhead - t_lo) <= 0 : fhead == t_lo);
       bool cut = false;                    // a DELIVER or ARRIVE may have cut a DECODE run
       if (__any_sync(FULL, dv)) {
         cut = true;
         bool lovf = false;
         if (dv) {
           if (coalesce) cut_run();
-          uint32_t* const ft = reinterpret_cast<uint32_t*>(my_ftick);
-          unsigned long long* const fb = reinterpret_cast<unsigned long long*>(my_fbody);
-          unsigned long long* ib = reinterpret_cast<unsigned long long*>(my_inbox);
-          for (;;) {
-            if (K1_UNLIKELY(in >= my_inbox_cap) && (!SPILL || in >= MI.inbox_cap)) { lovf = true; break; }
-            const unsigned long long body = fb[fh];
-            if (CLS && prio && rCls[body & 0xFFFFu]) {        // M27: class-1 ring
-              ib[my_inbox_cap + wrap_add(ih1, in1, my_inbox_cap)] = body;
-              ++in1;
-            } else {
-              const uint32_t k = in - (CLS ? in1 : 0u);
-              if (!SPILL || k < my_inbox_cap) {
-                const uint32_t at_idx = wrap_add(ih, k, my_inbox_cap);
-                ib[at_idx] = body;
-                if (my_kv) my_iready[at_idx] = my_fready[fh];        // emission + tau*ctx (M23 HINT)
-              } else {
-                reinterpret_cast<unsigned long long*>(gxa(MI.gx_inbox))[wrap_add(H->gh[0][lane], k - RS,
-                                                                                 MI.inbox_cap - RS)] = body;
-              }
-            }
-            ++in;
-            const uint32_t ofh = fh;
-            fh = wrap_add(fh, 1u, my_flight_cap);
-            if (SPILL && fn > my_flight_cap) {   // refill the vacated slot with the oldest extension entry
-              const uint32_t g0 = H->gh[1][lane];
-              ft[ofh] = reinterpret_cast<const uint32_t*>(gxa(MI.gx_ftick))[g0];
-              fb[ofh] = reinterpret_cast<const unsigned long long*>(gxa(MI.gx_fbody))[g0];
-              H->gh[1][lane] = (uint16_t)wrap_add(g0, 1u, MI.flight_cap - RS);
-            }
-            --fn;
-            ++cnt_deliv;
-            if (TRACE) trace_lane(TR_DELIVER, lane, rJ[body & 0xFFFFu], (uint32_t)(body >> 32) & 0xFFFFu);
-            if (fn == 0) break;
-            fhead = ft[fh];
-            if (fhead != t_lo) break;
-          }
+          lovf = deliver(false);
         }
         if (K1_UNLIKELY(__any_sync(FULL, lovf))) {
           if (TRACE) trace(TR_OVERFLOW, 0, 0, 0);
@@ -1271,6 +1392,9 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
       stg[34] = (uint32_t)h.sum_e2e_int; stg[35] = (uint32_t)(h.sum_e2e_int >> 32);
       stg[36] = v50i; stg[37] = v99i; stg[38] = h.good_int; stg[39] = h.gate_changes;
       stg[40] = select_changes; stg[41] = b50f | (b99f << 16); stg[42] = 0; stg[43] = 0;
+#ifdef K1_COUNT_ITERS
+      stg[42] = n_iter;
+#endif
       cst[24] = h.completed_int; cst[25] = h.rejected; cst[26] = h.sum_e2e_int; cst[27] = h.good_int;
       cst[0] = 1; cst[1] = status == SDAS_REPLICA_OK; cst[2] = 0; cst[3] = status == SDAS_REPLICA_TRUNCATED;
       cst[4] = admitted; cst[5] = dropped; cst[6] = completed; cst[7] = sum_e2e; cst[8] = sum_ff;
