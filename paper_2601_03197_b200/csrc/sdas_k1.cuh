@@ -79,7 +79,9 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
   // two-level rings (levels >= 1): a ring keeps its oldest RS entries in shared memory and
   // the rest in this warp's extension area of `work`; the my_*_cap registers hold the shared-memory sizes
   // min(capacity, RS) and the logical capacities (overflow, rule M14) are read from MI only past them
+  // (LEAN only: on level 1 the extra code pushed the hot loop out of the instruction cache, +45 % at config 3)
   constexpr bool LAZY = LV == 2;   // deliveries into a busy instance are not events
+  constexpr bool SILENT = LV == 2; // a RECV whose end changes nothing else is not an event
   constexpr bool SPILL = SPL;                          // a separate instantiation: grids whose rings fit whole
   static_assert(!SPL || LV >= 1, "two-level rings exist on the specialised levels only");   // never pay for it
   const uint32_t RS = SPILL ? Pk.ring_s : 0xFFFFFFFFu;
@@ -286,6 +288,18 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
       return dest != P.role[kv_role].first + rHome[slot] ? cd.kv_policy : 0u;
     };
 
+    // lane-local: a message due at tick x will enter this instance's inbox while it may be mid-run: end the
+    // run at the first step boundary >= x (the cut of M7's RECV-first START, applied when x becomes known)
+    auto cut_at = [&](uint32_t x) {
+      if (st != DECODE || runm <= 1u) return;
+      const uint32_t c = max(1u, MI.tau0 + MI.gamma * b);
+      const uint32_t rs = end_lo - runm * c;
+      const uint32_t mp = (x - rs + c - 1u) / c;
+      if (mp < runm) {
+        runm = mp;
+        end_lo = rs + mp * c;
+      }
+    };
     // M30 pacing gap of link l under this candidate (0 = unpaced)
     auto pace_gap = [&](uint32_t l) -> uint32_t { return cd.pace == 0xFFFFFFFFu ? P.link[l].gap : cd.pace; };
     // one message into destination `dest`'s in-flight ring (uniform; used by the serial paths)
@@ -330,6 +344,8 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
       if (lane == (int)dest) {
         if (fn == 0) fhead = tick;
         ++fn;
+        if (LAZY) cut_at(tick);                            // the delivery will not be an event of its own
+        if (SILENT && st == RECV && (int32_t)(tick - end_lo) < 0) runm = 1u;
       }
     };
 
@@ -434,23 +450,13 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
         if (K1_UNLIKELY(ovf)) return;
       }
       __syncwarp();                        // lane 0's ring writes precede the destinations' DELIVER reads
-      if (lane == 0 && role == ((modes >> 28) & 7u) && rFF[slot] == kUnsetFF) rFF[slot] = t - rA[slot];
+      // first feedback = the earliest first-output tick of the request's items (M13); a DECODE item may have
+      // recorded a later one in advance (LAZY), so take the minimum
+      if (lane == 0 && role == ((modes >> 28) & 7u)) rFF[slot] = min(rFF[slot], t - rA[slot]);
       if (P.inst[i].flags & 1u) { if (lane == (int)i) ++n_large; }
       item_done(slot);
     };
 
-    // lane-local: a message due at tick x will enter this instance's inbox while it may be mid-run: end the
-    // run at the first step boundary >= x (the cut of M7's RECV-first START, applied when x becomes known)
-    auto cut_at = [&](uint32_t x) {
-      if (st != DECODE || runm <= 1u) return;
-      const uint32_t c = max(1u, MI.tau0 + MI.gamma * b);
-      const uint32_t rs = end_lo - runm * c;
-      const uint32_t mp = (x - rs + c - 1u) / c;
-      if (mp < runm) {
-        runm = mp;
-        end_lo = rs + mp * c;
-      }
-    };
 
     // ---------------------------------------------------------------- phase COMPLETE: DECODE (M7, M9, M13)
     auto complete_decode = [&](uint32_t i) {
@@ -569,6 +575,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
                 if (fn == 0) fhead = tick;
                 fn += cnt;
                 if (LAZY) cut_at(tick);                    // the delivery will not be an event of its own
+                if (SILENT && st == RECV && (int32_t)(tick - end_lo) < 0) runm = 1u;   // re-arm a silent RECV
               }
             }
             __syncwarp();
@@ -689,6 +696,11 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
           }
         }
         --in;
+        // SILENT (runm = 0 while in RECV): a non-closing message whose RECV end leaves nothing to start (no
+        // inbox, wait or batch, no delivery due before it) only makes the instance idle: that happens at its
+        // next event instead (busy is integrated up to end_lo, a delivery emitted for before end_lo re-arms it)
+        runm = (SILENT && !((body >> 17) & 1u) && in == 0u && wn == 0u && b == 0u &&
+                (fn == 0u || (int32_t)(fhead - end_lo) >= 0)) ? 0u : 1u;
       }
       if (TRACE) trace(TR_RECV_START, i, rJ[__shfl_sync(FULL, slot, i)], __shfl_sync(FULL, cost32, i));
     };
@@ -700,7 +712,8 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
     // Returns the (possibly shorter) run length.  Lanes < nbat hold the batch words wA, wB.
     auto emit_ahead = [&](uint32_t i, const DRole& R, uint32_t nbat, uint32_t cost32, uint32_t m, uint32_t wA,
                           uint32_t wB) -> uint32_t {
-      const uint32_t l = R.out_link0, dk = P.link[l].dst;   // LEAN: role = instance
+      const uint32_t l = R.out_link0;                       // the destination role has one instance
+      const uint32_t dk = LEAN ? P.link[l].dst : P.role[P.link[l].dst].first;
       const DInst& D = P.inst[dk];
       uint32_t* const bat = at<uint32_t>(Wr, P.inst[i].off_batch);
       const bool act = lane < (int)nbat;
@@ -750,6 +763,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
           if (fn == 0) fhead = tick;
           fn += cnt;
           cut_at(tick);
+          if (SILENT && st == RECV && (int32_t)(tick - end_lo) < 0) runm = 1u;   // re-arm a silent RECV
         }
         fn_d += cnt;
         moved = true;
@@ -822,8 +836,9 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
       // AHEAD: the source role's inbox receives arrivals only, so its run is known up to the
       // next arrival; its emission points do not end the run -- their messages are emitted now, each with
       // its own emission tick, and the run ends at a finish / first feedback / arrival / window bound
+      const uint32_t ahead_dst = LEAN ? P.link[R.out_link0].dst : P.role[P.link[R.out_link0].dst].first;
       const bool ahead = LAZY && role == 0 && n_out == 1 && nbat > 0 && P.link[R.out_link0].net < cost32 &&
-                         nbat <= P.inst[P.link[R.out_link0].dst].flight_cap;
+                         (LEAN || P.role[P.link[R.out_link0].dst].n == 1) && nbat <= P.inst[ahead_dst].flight_cap;
       uint32_t m = 1;
       if (coalesce) {
         uint32_t sk = 0xFFFFFFFFu;
@@ -837,7 +852,12 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
           uint32_t lim = wA >> 16;                                      // out
           if (n_out > 0 && !ahead) lim = min(lim, wB >> 16);
           if (MAXOUT > 1 && n_out > 1) lim = min(lim, wD & 0xFFFFu);
-          sk = (role == ((modes >> 28) & 7u) && done == 0u) ? 1u : lim - done;
+          // LAZY: a sequence's first token lands at the end of this run's first step, known now, so the
+          // first feedback (M13: the earliest such tick of the request) is recorded now and is no stop
+          // point; rFF is read only when the request completes, after every one of its items finished
+          const bool first = role == ((modes >> 28) & 7u) && done == 0u;
+          if (LAZY && first) atomicMin(&rFF[wA & 0xFFFu], t + cost32 - rA[wA & 0xFFFu]);
+          sk = (!LAZY && first) ? 1u : lim - done;
         }
         m = __reduce_min_sync(FULL, sk);
         if (m > 1) {
@@ -1144,16 +1164,17 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
       if (!arr_more && nsys == 0) break;   // (arr_more == jn < N, kept in a register)
       // next tick: warp-min over 32-bit deltas (every pending event lies < 2^31 ticks ahead)
       // (branch-free: lanes that are not instances hold IDLE / empty state and contribute nothing)
-      uint32_t d = st != IDLE ? end_lo - t_lo : 0xFFFFFFFFu;
+      const bool quiet = SILENT && st == RECV && runm == 0u;   // a silent RECV: idle from end_lo on
+      uint32_t d = st != IDLE && !quiet ? end_lo - t_lo : 0xFFFFFFFFu;
       // LAZY: only idle instances (and any whose inbox could fill) wait for their deliveries as events
-      d = fn && (!LAZY || st == IDLE || in + fn > my_inbox_cap) ? min(d, fhead - t_lo) : d;
+      d = fn && (!LAZY || st == IDLE || quiet || in + fn > my_inbox_cap) ? min(d, fhead - t_lo) : d;
       const uint32_t d0 = min(nb_lo - t_lo, arr_near ? A_lo - t_lo : 0xFFFFFFFFu);
       d = lane == 0 ? min(d, d0) : d;
       d = __reduce_min_sync(FULL, d);
       if (K1_UNLIKELY(max_ticks && t + d > max_ticks)) { status = SDAS_REPLICA_TRUNCATED; break; }
       {  // integrate the piecewise-constant state over [t, t + d) (M15)
         const uint32_t Q = in + wn;
-        acc_busy += st != IDLE ? d : 0u;
+        acc_busy += st != IDLE ? (quiet ? min(d, (uint32_t)max(0, (int32_t)(end_lo - t_lo))) : d) : 0u;
         acc_qint += (unsigned long long)Q * d;
         acc_maxq = max(acc_maxq, Q);
         if (need_lint) acc_lint += (unsigned long long)(fn + Q + (st == RECV ? 1u : 0u) + b) * d;
@@ -1164,6 +1185,10 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
       // LAZY: messages delivered since the last event to a busy instance enter its inbox now -- before the
       // window split, and before COMPLETE's emissions test the in-flight rings (M14 counts undelivered only)
       if (LAZY && fn && (int32_t)(fhead - t_lo) < 0) deliver(true);
+      if (quiet && (int32_t)(end_lo - t_lo) <= 0) {        // the silent RECV has ended: the instance is idle
+        st = IDLE;
+        ++cnt_recv;
+      }
       if (K1_UNLIKELY(t_lo == nb_lo)) {  // phase 0 WINDOW
         close_window(false);
         nb_lo += W32;
