@@ -353,7 +353,7 @@ sdas_status plan(const sdas_pipeline* p, const sdas_grid* g, Plan& pl) {
   // a ring of capacity > RS keeps its oldest RS entries in shared memory, the rest in the
   // warp's extension area of `work`; levels >= 1 only -- level 0 keeps every ring whole)
   auto layout_for = [&](uint32_t RS) -> uint64_t {
-    uint64_t o = kHdrBytes;  // WarpHdr
+    uint64_t o = 256;  // WarpHdr
     const uint32_t R = p->request_cap;
     h.off_reqA = (uint32_t)o; o += 8ull * R;
     h.off_reqFF = (uint32_t)o; o += 8ull * R;              // exact u64 first-feedback latency (M13, M19)
@@ -388,8 +388,8 @@ sdas_status plan(const sdas_pipeline* p, const sdas_grid* g, Plan& pl) {
     }
     h.gx_per_warp = align_up(gx, 256);
     o = align_up(o, 16);
-    h.off_scratch = kHdrBytes;
-    return align_up(std::max<uint64_t>(o, kHdrBytes + (uint64_t)kScratchMin), 16);
+    h.off_scratch = 256;
+    return align_up(std::max<uint64_t>(o, 256 + (uint64_t)kScratchMin), 16);
   };
   h.off_warps = (uint32_t)align_up(sizeof(DParams), 128);
   const uint64_t smem_cap = 227 * 1024;

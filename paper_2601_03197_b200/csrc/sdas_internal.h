@@ -11,7 +11,6 @@ namespace sdas {
 
 constexpr unsigned long long kUnsetFF = ~0ull;   // first-feedback latency not yet observed (u64 slot)
 constexpr uint32_t kNever = 0xFFFFFFFFu;
-constexpr int kHdrBytes = 320;   // per-replica header (WarpHdr) at the start of a warp's shared region
 constexpr int kScratchMin = SDAS_NHIST * SDAS_NBINS * 4 + 256 * 4 + SDAS_SUMMARY_BYTES + SDAS_NCNT * 8;  // finalize scratch
 
 struct DInst {          // one instance, 80 B

@@ -165,10 +165,6 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
     // at the first step boundary >= its tick (RECV-first START, M7); flushm > 0 = a cut landed exactly
     // on a boundary of this tick and that many silent steps are applied before phase START.
     uint32_t runm = 1, flushm = 0;
-    // RECV chains (LEAN): while an instance is "quiet" (st == RECV, runm 0 or 2) it receives
-    // its planned chain of non-closing messages without events; runm 2 = a hard tick hch is known, at which
-    // the model needs an event again (a closing message's RECV start, or a RECV end with a message queued)
-    uint32_t hch = 0;
     // f2: class-1 (interactive) ring heads and counts; `in` / `wn` stay the totals over both rings
     uint32_t ih1 = 0, in1 = 0, wh1 = 0, wn1 = 0;
     const bool prio = CLS && cd.prio != 0;
@@ -304,24 +300,6 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
         end_lo = rs + mp * c;
       }
     };
-    // RECV cost of message `body` at this lane's instance (M7; svc DET -- chains require it)
-    auto recv_cost = [&](unsigned long long body) -> uint32_t {
-      const uint32_t c = MI.h + MI.beta * ((uint32_t)(body >> 32) & 0xFFFFu) + (((body >> 16) & F_OPENS) ? MI.alpha : 0u);
-      return max(1u, c);
-    };
-    // lane-local, quiet instance: the plan takes one more message delivered at T (ring order): chainable if it
-    // does not close its item and arrives at or after the planned RECVs end; else the hard tick is its RECV start
-    auto plan_add = [&](uint32_t T, unsigned long long body) {
-      if (runm != 0u) return;
-      const uint32_t ce = H->cend[lane];
-      if (((body >> 17) & 1u) || (int32_t)(T - ce) < 0) {
-        hch = (int32_t)(T - ce) < 0 ? ce : T;
-        runm = 2u;
-      } else {
-        H->cend[lane] = T + recv_cost(body);
-        ++H->nch[lane];
-      }
-    };
     // M30 pacing gap of link l under this candidate (0 = unpaced)
     auto pace_gap = [&](uint32_t l) -> uint32_t { return cd.pace == 0xFFFFFFFFu ? P.link[l].gap : cd.pace; };
     // one message into destination `dest`'s in-flight ring (uniform; used by the serial paths)
@@ -367,7 +345,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
         if (fn == 0) fhead = tick;
         ++fn;
         if (LAZY) cut_at(tick);                            // the delivery will not be an event of its own
-        if (SILENT && st == RECV && runm != 1u) plan_add(tick, make_body(slot, flags, tokens, n_in));
+        if (SILENT && st == RECV && (int32_t)(tick - end_lo) < 0) runm = 1u;
       }
     };
 
@@ -579,8 +557,6 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
                 return;
               }
               const uint32_t tick = __shfl_sync(FULL, my_tick, __ffs(grp) - 1);   // group's first message
-              const unsigned long long body0 =
-                  SILENT ? __shfl_sync(FULL, make_body(slot, flags, tokens, n_in), __ffs(grp) - 1) : 0ull;
               if ((grp >> lane) & 1u) {
                 const uint32_t k = fn_d + __popc(grp & lanemask_lt()), pm_d = min(D.flight_cap, RS);
                 if (!SPILL || k < pm_d) {
@@ -599,10 +575,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
                 if (fn == 0) fhead = tick;
                 fn += cnt;
                 if (LAZY) cut_at(tick);                    // the delivery will not be an event of its own
-                if (SILENT && st == RECV && runm != 1u) {   // a quiet instance plans the group's first message;
-                  plan_add(tick, body0);                    // the rest arrive before its RECV ends: hard
-                  if (cnt > 1u && runm == 0u) { hch = H->cend[lane]; runm = 2u; }
-                }
+                if (SILENT && st == RECV && (int32_t)(tick - end_lo) < 0) runm = 1u;   // re-arm a silent RECV
               }
             }
             __syncwarp();
@@ -723,33 +696,11 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
           }
         }
         --in;
-        // SILENT: a non-closing message whose RECV leaves nothing else to start (no inbox, wait or batch) opens
-        // a RECV chain (quiet): the RECV ends and the following non-closing messages' RECVs (each starting at
-        // its delivery tick, after the previous one ended) are no events; the plan (cend, nch) covers the
-        // messages already in flight and grows as more are emitted, until a hard tick
-        runm = 1u;
-        if (SILENT && !((body >> 17) & 1u) && in == 0u && wn == 0u && b == 0u && !(MI.flags & 2u)) {
-          runm = 0u;
-          ++cnt_recv;                                      // chained RECVs are counted when they start
-          H->cend[lane] = end_lo;
-          H->nch[lane] = 0;
-          const uint32_t* const ft = reinterpret_cast<const uint32_t*>(my_ftick);
-          const unsigned long long* const fb = reinterpret_cast<const unsigned long long*>(my_fbody);
-          for (uint32_t k = 0; k < fn && runm == 0u; ++k) {
-            uint32_t tk;
-            unsigned long long bk;
-            if (!SPILL || k < my_flight_cap) {
-              const uint32_t idx = wrap_add(fh, k, my_flight_cap);
-              tk = ft[idx];
-              bk = fb[idx];
-            } else {
-              const uint32_t gi = wrap_add(H->gh[1][lane], k - RS, MI.flight_cap - RS);
-              tk = reinterpret_cast<const uint32_t*>(gxa(MI.gx_ftick))[gi];
-              bk = reinterpret_cast<const unsigned long long*>(gxa(MI.gx_fbody))[gi];
-            }
-            plan_add(tk, bk);
-          }
-        }
+        // SILENT (runm = 0 while in RECV): a non-closing message whose RECV end leaves nothing to start (no
+        // inbox, wait or batch, no delivery due before it) only makes the instance idle: that happens at its
+        // next event instead (busy is integrated up to end_lo, a delivery emitted for before end_lo re-arms it)
+        runm = (SILENT && !((body >> 17) & 1u) && in == 0u && wn == 0u && b == 0u &&
+                (fn == 0u || (int32_t)(fhead - end_lo) >= 0)) ? 0u : 1u;
       }
       if (TRACE) trace(TR_RECV_START, i, rJ[__shfl_sync(FULL, slot, i)], __shfl_sync(FULL, cost32, i));
     };
@@ -783,7 +734,6 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
         const uint32_t cnt = __popc(em);
         if (fn_d + cnt > D.flight_cap) { m = k; break; }   // no room next to the ring's content: end here
         const uint32_t tick = t_lo + k * cost32 + net;
-        unsigned long long mybody = 0;
         if (s == k) {
           const bool tm = mode == SDAS_TOKEN;
           const uint32_t tokens = nxt - prev;
@@ -791,7 +741,6 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
           const uint32_t n_in = tm ? out : tokens;
           const uint32_t q = fn_d + __popc(em & lanemask_lt());
           const unsigned long long body = make_body(slot, flags, tokens, n_in);
-          mybody = body;
           if (!SPILL || q < pm_d) {
             const uint32_t idx = wrap_add(fh_d, q, pm_d);
             at<uint32_t>(Wr, D.off_ftick)[idx] = tick;
@@ -810,15 +759,11 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
             nxt = min(nxt + chunk, out);
           }
         }
-        const unsigned long long body0 = __shfl_sync(FULL, mybody, __ffs(em) - 1);
         if (lane == (int)dk) {
           if (fn == 0) fhead = tick;
           fn += cnt;
           cut_at(tick);
-          if (SILENT && st == RECV && runm != 1u) {        // a quiet destination plans the step's messages
-            plan_add(tick, body0);
-            if (cnt > 1u && runm == 0u) { hch = H->cend[lane]; runm = 2u; }
-          }
+          if (SILENT && st == RECV && (int32_t)(tick - end_lo) < 0) runm = 1u;   // re-arm a silent RECV
         }
         fn_d += cnt;
         moved = true;
@@ -1207,43 +1152,6 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
       }
     };
 
-    // lane-local, quiet instance: start the planned RECVs of the chainable head messages
-    // delivered before now (incl: or at now), each at its own delivery tick; busy time up to now is added
-    // here (the integration step covers the rest); at the hard tick the plan is done and the instance idles
-    auto chain_run = [&](bool incl) {
-      uint32_t nc = H->nch[lane];
-      if (nc) {
-        uint32_t* const ft = reinterpret_cast<uint32_t*>(my_ftick);
-        unsigned long long* const fb = reinterpret_cast<unsigned long long*>(my_fbody);
-        while (nc && (int32_t)(fhead - t_lo) < (incl ? 1 : 0)) {
-          const unsigned long long body = fb[fh];
-          const uint32_t c = recv_cost(body);
-          if ((body >> 16) & F_OPENS) {
-            const uint32_t sl = (uint32_t)(body & 0xFFFFu);
-            rNit[sl] = (uint16_t)(rNit[sl] + 1u);
-          }
-          end_lo = fhead + c;
-          cur = body;
-          ++cnt_recv;
-          ++cnt_deliv;
-          acc_busy += min(c, t_lo - fhead);
-          const uint32_t ofh = fh;
-          fh = wrap_add(fh, 1u, my_flight_cap);
-          if (SPILL && fn > my_flight_cap) {   // refill the vacated slot with the oldest extension entry
-            const uint32_t g0 = H->gh[1][lane];
-            ft[ofh] = reinterpret_cast<const uint32_t*>(gxa(MI.gx_ftick))[g0];
-            fb[ofh] = reinterpret_cast<const unsigned long long*>(gxa(MI.gx_fbody))[g0];
-            H->gh[1][lane] = (uint16_t)wrap_add(g0, 1u, MI.flight_cap - RS);
-          }
-          --fn;
-          --nc;
-          if (fn) fhead = ft[fh];
-        }
-        H->nch[lane] = (uint16_t)nc;
-      }
-      if (runm == 2u && (int32_t)(t_lo - hch) >= 0) st = IDLE;   // planned RECVs all ended by hch
-    };
-
     // ---------------------------------------------------------------- event loop (M12)
 #ifdef K1_COUNT_ITERS
     uint32_t n_iter = 0;   // experiment builds only (tools/iters.py): event-loop iterations -> summary word 42
@@ -1256,10 +1164,10 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
       if (!arr_more && nsys == 0) break;   // (arr_more == jn < N, kept in a register)
       // next tick: warp-min over 32-bit deltas (every pending event lies < 2^31 ticks ahead)
       // (branch-free: lanes that are not instances hold IDLE / empty state and contribute nothing)
-      const bool quiet = SILENT && st == RECV && runm != 1u;   // in a RECV chain: its own event is the hard tick
-      uint32_t d = st != IDLE && !quiet ? end_lo - t_lo : (quiet && runm == 2u ? hch - t_lo : 0xFFFFFFFFu);
+      const bool quiet = SILENT && st == RECV && runm == 0u;   // a silent RECV: idle from end_lo on
+      uint32_t d = st != IDLE && !quiet ? end_lo - t_lo : 0xFFFFFFFFu;
       // LAZY: only idle instances (and any whose inbox could fill) wait for their deliveries as events
-      d = fn && (!LAZY || st == IDLE || in + fn > my_inbox_cap) ? min(d, fhead - t_lo) : d;
+      d = fn && (!LAZY || st == IDLE || quiet || in + fn > my_inbox_cap) ? min(d, fhead - t_lo) : d;
       const uint32_t d0 = min(nb_lo - t_lo, arr_near ? A_lo - t_lo : 0xFFFFFFFFu);
       d = lane == 0 ? min(d, d0) : d;
       d = __reduce_min_sync(FULL, d);
@@ -1276,8 +1184,11 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
       t_lo += d;
       // LAZY: messages delivered since the last event to a busy instance enter its inbox now -- before the
       // window split, and before COMPLETE's emissions test the in-flight rings (M14 counts undelivered only)
-      if (quiet) chain_run(false);
-      if (LAZY && fn && (int32_t)(fhead - t_lo) < 0 && !(quiet && H->nch[lane])) deliver(true);
+      if (LAZY && fn && (int32_t)(fhead - t_lo) < 0) deliver(true);
+      if (quiet && (int32_t)(end_lo - t_lo) <= 0) {        // the silent RECV has ended: the instance is idle
+        st = IDLE;
+        ++cnt_recv;
+      }
       if (K1_UNLIKELY(t_lo == nb_lo)) {  // phase 0 WINDOW
         close_window(false);
         nb_lo += W32;
@@ -1286,7 +1197,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
       }
       // phase 1 COMPLETE (instance order)
       // (lanes >= n_inst stay IDLE with empty rings: no is_inst test needed in the phase votes)
-      const bool done_here = st != IDLE && end_lo == t_lo && !(SILENT && st == RECV && runm != 1u);
+      const bool done_here = st != IDLE && end_lo == t_lo;
       uint32_t cm = __ballot_sync(FULL, done_here);
       if (cm) {
         const uint32_t rm = __ballot_sync(FULL, done_here && st == RECV);
@@ -1309,8 +1220,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
         bool lovf = false;
         if (dv) {
           if (coalesce) cut_run();
-          if (SILENT && st == RECV && runm != 1u && H->nch[lane]) chain_run(true);   // a chained one, due now
-          else lovf = deliver(false);
+          lovf = deliver(false);
         }
         if (K1_UNLIKELY(__any_sync(FULL, lovf))) {
           if (TRACE) trace(TR_OVERFLOW, 0, 0, 0);

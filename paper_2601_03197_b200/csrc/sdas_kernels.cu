@@ -45,10 +45,8 @@ struct WarpHdr {                        // per-replica counters owned by lane 0 
                                                  // cell: (i*K + k)*C + c
   unsigned long long pace_free[8];               // f4 M30: per link, earliest tick of the next dispatch
   uint16_t gh[3][8];   // two-level rings: head of the inbox / in-flight / wait extension per instance
-  uint32_t cend[8];    // RECV chains: per instance, end tick of the last planned chained RECV
-  uint16_t nch[8];     //   and the number of chainable messages at the head of its in-flight ring
 };
-static_assert(sizeof(WarpHdr) <= kHdrBytes, "WarpHdr");
+static_assert(sizeof(WarpHdr) <= 256, "WarpHdr");
 
 // ------------------------------------------------------------------------------ primitives
 // Philox4x32-10 (rule M2): ctr = (c0, c1, c2, c3), key = (k0, k1); returns words 0 and 1.
