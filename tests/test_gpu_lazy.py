@@ -1,4 +1,5 @@
-"""LEAN K1's lazy deliveries and emit-ahead source runs against the oracle and against the
+"""LEAN K1's lazy deliveries, emit-ahead source runs, RECV chains and advance first feedback
+against the oracle and against the
 generic kernel (which delivers every message as its own event and ends every run at an emission point):
 P2-X / P2-SPEC variants that exercise every branch -- TOKEN / FUNCTION / BATCH, deep batches (B = 32) whose
 emit-ahead steps do not fit the destination's in-flight ring (room-limited runs), in-flight rings smaller
@@ -33,7 +34,7 @@ CANDS = [W.static("token"), W.static("function"), W.static("batch"), W.adaptive(
 
 
 @pytest.mark.parametrize("variant", ["base", "b32_room", "tiny_flight", "slow_net", "small_inbox", "det_boundary",
-                                     "spec_chunk1", "series"])
+                                     "spec_chunk1", "series", "slow_recv", "fast_recv", "tiny_inbox"])
 def test_lazy_and_ahead_variants(variant):
     p = W.p2_x()
     g = W.grid(copy.deepcopy(CANDS), [W.poisson(m) for m in (3994000, 998500, 469882, 347304)], n_seeds=3,
@@ -51,6 +52,14 @@ def test_lazy_and_ahead_variants(variant):
         g["arrivals"] = [[W.det(16000 * k)] for k in (40, 100, 250)]
     elif variant == "spec_chunk1":     # P2-SPEC with TOKEN(1): an emission every step
         p = W.p2_spec(mode="token", chunk=1, n_functions=4)
+    elif variant == "slow_recv":       # chunk RECVs longer than the chunk spacing: chains break (hard ticks)
+        p["roles"][1]["cost"]["h"] = 60000
+    elif variant == "fast_recv":       # cheap chunk RECVs: long chains of non-closing chunks
+        p["roles"][1]["cost"].update(h=500, beta=5)
+        p["links"][0]["chunk"] = 2
+    elif variant == "tiny_inbox":      # hard messages queue behind chains into a 3-slot inbox: overflow ticks
+        p["roles"][1]["inbox_cap"] = 3
+        p["roles"][1]["cost"]["h"] = 30000
     elif variant == "series":
         g["series_stride"], g["series_slots"], g["series_windows"] = 7, 9, 200
         series = True
