@@ -218,12 +218,6 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
     };
 
     // ---------------------------------------------------------------- arrivals (M4, M5)
-    auto advance_epoch = [&]() {
-      ++mm_k;
-      const uint2 w = philox(mm_k, s_coord, 4u << 16, 0u, key0, key1);
-      const unsigned long long d = exp_sample((mm_k & 1) ? ad.soj1 : ad.soj0, w.x);
-      mm_end += d > 0 ? d : 1ull;
-    };
     auto gen = [&](uint32_t j, unsigned long long A_prev) {
       const uint32_t kind = ad.kind;
       if (kind == SDAS_POISSON) {
@@ -234,15 +228,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
       } else if (kind == SDAS_LIST) {
         A_next = reinterpret_cast<const unsigned long long*>(blob + ad.list_off)[j];
       } else {  // MMPP2: restart at epoch edges
-        unsigned long long tt = A_prev;
-        while (mm_end <= tt) advance_epoch();
-        for (;;) {
-          const uint2 w = philox(j, s_coord, 1u << 16, mm_k, key0, key1);
-          const unsigned long long gg = exp_sample((mm_k & 1) ? ad.gap1 : ad.gap0, w.x);
-          if (tt + gg < mm_end) { A_next = tt + gg; break; }
-          tt = mm_end;
-          advance_epoch();
-        }
+        A_next = mmpp_next(j, s_coord, A_prev, mm_k, mm_end, ad, key0, key1);
       }
       const uint4 w = philox4(j, s_coord, 2u << 16, 0u, key0, key1);
       P_next = uni(ad.p_lo, ad.p_hi, w.x);

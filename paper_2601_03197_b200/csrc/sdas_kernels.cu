@@ -133,6 +133,32 @@ __device__ __forceinline__ unsigned long long warp_sum64(unsigned long long v) {
   return v;
 }
 
+// MMPP-2 next arrival after A_prev (rule M4: restart at epoch edges; epoch k lasts max(1, EXP(D_{k mod 2}))).
+// Out of line: K1's hot loop sits at the instruction-cache limit and Poisson grids never
+// take this path.  mm_k / mm_end: the current epoch and its end (updated).
+#ifdef K1_MMPP_NOINLINE
+__device__ __noinline__
+#else
+__device__ __forceinline__
+#endif
+unsigned long long mmpp_next(uint32_t j, uint32_t s_coord, unsigned long long A_prev, uint32_t& mm_k,
+                                                unsigned long long& mm_end, const DArr& ad, uint32_t key0,
+                                                uint32_t key1) {
+  unsigned long long tt = A_prev;
+  for (;;) {
+    while (mm_end <= tt) {
+      ++mm_k;
+      const uint2 w = philox(mm_k, s_coord, 4u << 16, 0u, key0, key1);
+      const unsigned long long d = exp_sample((mm_k & 1) ? ad.soj1 : ad.soj0, w.x);
+      mm_end += d > 0 ? d : 1ull;
+    }
+    const uint2 w = philox(j, s_coord, 1u << 16, mm_k, key0, key1);
+    const unsigned long long gg = exp_sample((mm_k & 1) ? ad.gap1 : ad.gap0, w.x);
+    if (tt + gg < mm_end) return tt + gg;
+    tt = mm_end;
+  }
+}
+
 // ------------------------------------------------------------------------------ K1
 template <typename T>
 __device__ __forceinline__ T* at(uint8_t* base, uint32_t off) {

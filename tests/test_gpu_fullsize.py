@@ -44,7 +44,7 @@ def test_config2_full_size_sampled():
     summ = res.summary()
     R = W.grid_size(g)
     assert len(summ) == R == 1 << 20
-    ids = np.asarray(W.sample_ids(R, 384), dtype=np.uint64)
+    ids = np.asarray(W.sample_ids(R, 4096), dtype=np.uint64)         # 4096 sampled replicas
     o = oracle.simulate(p, g, ids=ids, records=False, hists=False)
     compare_summaries(summ[ids.astype(np.int64)], o["summary"], where="config2 sample")
     cnt, _ = res.cells()
@@ -52,6 +52,25 @@ def test_config2_full_size_sampled():
     assert int(cnt[:, F["n_replicas"]].sum()) == R
     assert int(cnt[:, F["arrivals"]].sum()) == int(summ["arrivals"].astype(np.int64).sum())
     assert int(cnt[:, F["mode_switches"]].sum()) == int(summ["mode_switches"].astype(np.int64).sum())
+
+
+def test_config2_full_size_records_sampled():
+    """The bench's config-2 launch with exact per-request records on (FLAG_RECORDS, 8.4 GB): every record of
+    1024 sampled replicas (e2e and first feedback of each of their 1000 requests) equals the oracle's."""
+    import torch
+    p, g = W.config2(series_stride=0)
+    P = sdas.Pipeline(p)
+    gv = sdas.GridView(p, g, flags=sdas.FLAG_RECORDS)
+    res = sdas.control_sweep(P, gv, objective="p99_e2e")
+    torch.cuda.synchronize()
+    ids = np.asarray(W.sample_ids(W.grid_size(g), 1024), dtype=np.int64)
+    o = oracle.simulate(p, g, ids=ids.astype(np.uint64), records=True, hists=False)
+    N = g["n_requests"]
+    rec = res.t["records"].view(torch.int64).view(-1, N)[torch.as_tensor(ids, device=res.t["records"].device)]
+    rec = rec.cpu().numpy().view(np.uint32).reshape(len(ids), N, 2)
+    summ = res.summary()[ids]
+    compare_summaries(summ, o["summary"], where="config2 records sample")
+    compare_records(rec, o["records"], summ)
 
 
 def test_max_requests_and_full_batches():
@@ -84,7 +103,7 @@ def test_full_size_grid_sampled(cfg):
     torch.cuda.synchronize()
     summ = res.summary()
     assert len(summ) == n_groups * C == 1 << 20
-    local = np.asarray(W.sample_ids(len(summ), 256), dtype=np.int64)
+    local = np.asarray(W.sample_ids(len(summ), 2048), dtype=np.int64)
     ids = (local + g0 * C).astype(np.uint64)
     o = oracle.simulate(p, g, ids=ids, records=False, hists=False)
     compare_summaries(summ[local], o["summary"], where="%s slice sample" % cfg)
