@@ -498,7 +498,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
             if (mode == SDAS_FUNCTION) {
               ++fidx;
               const uint32_t Fp = min(R.n_functions, out);
-              nx = min((uint32_t)(((unsigned long long)(fidx + 1u) * out) / Fp), 0xFFFFu);
+              nx = ((fidx + 1u) * out) / Fp   /* < 2^24: fidx < 256, out < 2^16 */;
             } else if (tm) {
               nx = min(next + P.link[l].chunk, out);
             }
@@ -740,7 +740,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
           prev = nxt;
           if (mode == SDAS_FUNCTION) {
             ++fidx;
-            nxt = min((uint32_t)(((unsigned long long)(fidx + 1u) * out) / Fp), 0xFFFFu);
+            nxt = ((fidx + 1u) * out) / Fp   /* < 2^24: fidx < 256, out < 2^16 */;
           } else {                                          // TOKEN (BATCH emits at the end only)
             nxt = min(nxt + chunk, out);
           }
@@ -1261,7 +1261,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
 
     // ---------------------------------------------------------------- finalize (M18, M19)
     uint8_t* const sum_out = summary + x * SDAS_SUMMARY_BYTES;
-    const unsigned long long cell = ((g / Pk.S) % (Pk.I * (unsigned long long)Pk.K)) * C + c;
+    const unsigned long long cell = H->cell;                 // (i*K + k)*C + c, computed at the replica's start
     uint32_t* const stg = scratch + SDAS_NHIST * SDAS_NBINS + 256;   // 44 summary words, then counters
     unsigned long long* const cst = reinterpret_cast<unsigned long long*>(stg + SDAS_SUMMARY_BYTES / 4);
     __syncwarp();
