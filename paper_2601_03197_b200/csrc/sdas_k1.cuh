@@ -1145,6 +1145,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
     for (;;) {
 #ifdef K1_COUNT_ITERS
       ++n_iter;
+      uint32_t itype = 0;   // bit 0 WINDOW, 1 COMPLETE RECV, 2 COMPLETE DECODE, 3 DELIVER, 4 ARRIVE, 5/6 START RECV/DECODE
 #endif
       __syncwarp();
       if (!arr_more && nsys == 0) break;   // (arr_more == jn < N, kept in a register)
@@ -1154,32 +1155,46 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
       uint32_t d = st != IDLE && !quiet ? end_lo - t_lo : 0xFFFFFFFFu;
       // LAZY: only idle instances (and any whose inbox could fill) wait for their deliveries as events
       d = fn && (!LAZY || st == IDLE || quiet || in + fn > my_inbox_cap) ? min(d, fhead - t_lo) : d;
-      const uint32_t d0 = min(nb_lo - t_lo, arr_near ? A_lo - t_lo : 0xFFFFFFFFu);
+      // a window boundary is an event of its own only while the next arrival is too far for 32-bit deltas
+      // (or under max_ticks, whose truncation test must see every boundary before it, as M12 orders them)
+      const uint32_t d0 = min(arr_near ? A_lo - t_lo : 0xFFFFFFFFu, (!arr_near || max_ticks) ? nb_lo - t_lo : 0xFFFFFFFFu);
       d = lane == 0 ? min(d, d0) : d;
       d = __reduce_min_sync(FULL, d);
       if (K1_UNLIKELY(max_ticks && t + d > max_ticks)) { status = SDAS_REPLICA_TRUNCATED; break; }
-      {  // integrate the piecewise-constant state over [t, t + d) (M15)
+      // integrate the piecewise-constant state over [t, t + dd) (M15); a zero-length piece adds nothing
+      auto integrate = [&](uint32_t dd) {
         const uint32_t Q = in + wn;
-        acc_busy += st != IDLE ? (quiet ? min(d, (uint32_t)max(0, (int32_t)(end_lo - t_lo))) : d) : 0u;
-        acc_qint += (unsigned long long)Q * d;
-        acc_maxq = max(acc_maxq, Q);
-        if (need_lint) acc_lint += (unsigned long long)(fn + Q + (st == RECV ? 1u : 0u) + b) * d;
-      }
-      int_nsys += (unsigned long long)nsys * d;
-      t += d;
-      t_lo += d;
-      // LAZY: messages delivered since the last event to a busy instance enter its inbox now -- before the
-      // window split, and before COMPLETE's emissions test the in-flight rings (M14 counts undelivered only)
-      if (LAZY && fn && (int32_t)(fhead - t_lo) < 0) deliver(true);
-      if (quiet && (int32_t)(end_lo - t_lo) <= 0) {        // the silent RECV has ended: the instance is idle
-        st = IDLE;
-        ++cnt_recv;
-      }
-      if (K1_UNLIKELY(t_lo == nb_lo)) {  // phase 0 WINDOW
+        acc_busy += st != IDLE ? (quiet ? min(dd, (uint32_t)max(0, (int32_t)(end_lo - t_lo))) : dd) : 0u;
+        acc_qint += (unsigned long long)Q * dd;
+        if (dd) acc_maxq = max(acc_maxq, Q);
+        if (need_lint) acc_lint += (unsigned long long)(fn + Q + (st == RECV ? 1u : 0u) + b) * dd;
+        int_nsys += (unsigned long long)nsys * dd;
+        t += dd;
+        t_lo += dd;
+      };
+      // phase 0 WINDOW for every boundary on the way to t + d: nothing happens between two events, so a
+      // window closes when the state is integrated up to its boundary, and its decisions apply from there on
+      uint32_t rem = d;
+      while (K1_UNLIKELY(rem >= nb_lo - t_lo)) {
+        const uint32_t dd = nb_lo - t_lo;
+        integrate(dd);
+        rem -= dd;
+        if (LAZY && fn && (int32_t)(fhead - t_lo) < 0) deliver(true);   // their inbox time before the boundary
+#ifdef K1_COUNT_ITERS
+        itype |= 1u;
+#endif
         close_window(false);
         nb_lo += W32;
         ++wk;
         if (!arr_near && arr_more) arr_near = A_next - t < 0x80000000ull;
+      }
+      integrate(rem);
+      // LAZY: messages delivered since the last event to a busy instance enter its inbox now -- before
+      // COMPLETE's emissions test the in-flight rings (M14 counts undelivered only)
+      if (LAZY && fn && (int32_t)(fhead - t_lo) < 0) deliver(true);
+      if (quiet && (int32_t)(end_lo - t_lo) <= 0) {        // the silent RECV has ended: the instance is idle
+        st = IDLE;
+        ++cnt_recv;
       }
       // phase 1 COMPLETE (instance order)
       // (lanes >= n_inst stay IDLE with empty rings: no is_inst test needed in the phase votes)
@@ -1187,6 +1202,9 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
       uint32_t cm = __ballot_sync(FULL, done_here);
       if (cm) {
         const uint32_t rm = __ballot_sync(FULL, done_here && st == RECV);
+#ifdef K1_COUNT_ITERS
+        itype |= (rm ? 2u : 0u) | ((cm & ~rm) ? 4u : 0u);
+#endif
         do {
           const int i = __ffs(cm) - 1;
           cm &= cm - 1;
@@ -1202,6 +1220,9 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
       const bool dv = fn > 0 && (LAZY ? (int32_t)(fhead - t_lo) <= 0 : fhead == t_lo);
       bool cut = false;                    // a DELIVER or ARRIVE may have cut a DECODE run
       if (__any_sync(FULL, dv)) {
+#ifdef K1_COUNT_ITERS
+        itype |= 8u;
+#endif
         cut = true;
         bool lovf = false;
         if (dv) {
@@ -1217,6 +1238,9 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
       }
       // phase 3 ARRIVE (increasing j)
       if (K1_UNLIKELY(arr_near && A_lo == t_lo)) {
+#ifdef K1_COUNT_ITERS
+        itype |= 16u;
+#endif
         cut = true;
         do {
           arrive();
@@ -1250,6 +1274,9 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
       uint32_t sm = __ballot_sync(FULL, can);
       if (sm) {
         const uint32_t recvm = __ballot_sync(FULL, can && in != 0u);
+#ifdef K1_COUNT_ITERS
+        itype |= (recvm ? 32u : 0u) | ((sm & ~recvm) ? 64u : 0u);
+#endif
         do {
           const int i = __ffs(sm) - 1;
           sm &= sm - 1;
@@ -1257,6 +1284,13 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
           else start_decode((uint32_t)i);
         } while (sm);
       }
+#ifdef K1_COUNT_ITERS
+      if (lane == 0) {    // work->pad[1 + f]: iterations with flag f; pad[8 + f]: iterations whose only flag is f
+        for (int f = 0; f < 7; ++f)
+          if ((itype >> f) & 1u) atomicAdd(&work->pad[1 + f], 1ull);
+        if (__popc(itype) == 1) atomicAdd(&work->pad[8 + __ffs(itype) - 1], 1ull);
+      }
+#endif
     }
 
     // ---------------------------------------------------------------- finalize (M18, M19)

@@ -28,3 +28,9 @@ for name, fl in (("auto", 0), ("generic", sdas.FLAG_GENERIC)):
     per_rate = it.reshape(I, -1).mean(1)
     print("  iterations/replica by rate:", " ".join("%.0f" % x for x in per_rate))
     print("  msg/replica by rate:", " ".join("%.0f" % x for x in (s["arrivals"] + s["deliveries"]).astype(np.int64).reshape(I, -1).mean(1)))
+    w = r.t["work"][: 8 * 32].cpu().numpy().view(np.uint64)
+    names = ["WINDOW", "COMPLETE_RECV", "COMPLETE_DECODE", "DELIVER", "ARRIVE", "START_RECV", "START_DECODE"]
+    tot_it = it.sum()
+    # work words: [0] replica counter, [1 + 1 + f] = pad[1 + f] iterations with flag f, [1 + 8 + f] only flag f
+    print("  iterations with flag (share):", ", ".join("%s %.3f" % (n, w[2 + f] / tot_it) for f, n in enumerate(names)))
+    print("  iterations with only that flag:", ", ".join("%s %.3f" % (n, w[9 + f] / tot_it) for f, n in enumerate(names)))
