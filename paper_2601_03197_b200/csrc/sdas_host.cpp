@@ -10,6 +10,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -410,6 +411,9 @@ sdas_status plan(const sdas_pipeline* p, const sdas_grid* g, Plan& pl) {
         bps = std::min(bps, (int)(64 / wpb));
       }
       const uint64_t tot = (uint64_t)bps * wpb;
+      if (getenv("SDAS_PLAN_DEBUG"))                   // experiments: the occupancy the planner sees
+        fprintf(stderr, "plan: ring_s %u per_warp %llu wpb %u block_smem %llu -> blocks/SM %d\n", rs,
+                (unsigned long long)per_warp, wpb, (unsigned long long)sb, bps);
       if (tot >= best_tot) { best_tot = tot; bw = wpb; bb = (uint32_t)bps; }
     }
     return best_tot;
