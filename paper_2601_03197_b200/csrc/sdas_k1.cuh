@@ -1198,10 +1198,14 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
       }
       // phase 1 COMPLETE (instance order)
       // (lanes >= n_inst stay IDLE with empty rings: no is_inst test needed in the phase votes)
+      // the three phase votes are independent (COMPLETE's emissions are due after now and never change a
+      // due in-flight head), so they are issued back to back instead of each behind the previous phase
       const bool done_here = st != IDLE && end_lo == t_lo;
       uint32_t cm = __ballot_sync(FULL, done_here);
+      const uint32_t rm = __ballot_sync(FULL, done_here && st == RECV);
+      const bool dv = fn > 0 && (LAZY ? (int32_t)(fhead - t_lo) <= 0 : fhead == t_lo);
+      const uint32_t dvm = __ballot_sync(FULL, dv);
       if (cm) {
-        const uint32_t rm = __ballot_sync(FULL, done_here && st == RECV);
 #ifdef K1_COUNT_ITERS
         itype |= (rm ? 2u : 0u) | ((cm & ~rm) ? 4u : 0u);
 #endif
@@ -1217,9 +1221,8 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
       // phase 2 DELIVER (per destination instance, FIFO; lane = instance).  LAZY: a busy destination's
       // deliveries are not events of their own; they are moved here at its next event, with
       // the inbox time they missed added to the window integral
-      const bool dv = fn > 0 && (LAZY ? (int32_t)(fhead - t_lo) <= 0 : fhead == t_lo);
       bool cut = false;                    // a DELIVER or ARRIVE may have cut a DECODE run
-      if (__any_sync(FULL, dv)) {
+      if (dvm) {
 #ifdef K1_COUNT_ITERS
         itype |= 8u;
 #endif
@@ -1272,8 +1275,8 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
       __syncwarp();                        // wait-ring / request-table writes of this tick are visible
       const bool can = st == IDLE && (in | wn | b) != 0u;
       uint32_t sm = __ballot_sync(FULL, can);
+      const uint32_t recvm = __ballot_sync(FULL, can && in != 0u);
       if (sm) {
-        const uint32_t recvm = __ballot_sync(FULL, can && in != 0u);
 #ifdef K1_COUNT_ITERS
         itype |= (recvm ? 32u : 0u) | ((sm & ~recvm) ? 64u : 0u);
 #endif

@@ -146,3 +146,36 @@ def test_pacing_gap_knob():
     assert e.value.code == sdas.E_OUT_OF_RANGE
     P.reset("link:0->1/pacing_gap")
     assert P.get("link:0->1/pacing_gap") == 0
+
+
+def test_layout_two_level_rings_and_cell_series():
+    # FLAG_SPILL forces the 32-entry shared ring bound on specialised levels; level-0 grids
+    # (here: truncation) keep whole rings; the extension area lives in `work`; FLAG_CELL_SERIES sizes the
+    # cell-summed series buffer (n_cells x series_windows x n_instances x 64 B)
+    p, g = W.config3(n_seeds=2, n_requests=100)
+    P = sdas.Pipeline(p)
+    whole = sdas.results_layout(P, sdas.GridView(p, g, flags=sdas.FLAG_GENERIC))
+    assert whole.k1_variant == 0 and whole.ring_s == 0xFFFFFFFF
+    sp = sdas.results_layout(P, sdas.GridView(p, g, flags=sdas.FLAG_SPILL))
+    assert sp.k1_variant == 1 and sp.ring_s == 32
+    assert sp.smem_per_replica < whole.smem_per_replica and sp.work_bytes > whole.work_bytes
+    g["series_windows"] = 50
+    cs = sdas.results_layout(P, sdas.GridView(p, g, flags=sdas.FLAG_CELL_SERIES))
+    n_inst = sum(r["n_instances"] for r in p["roles"])
+    assert cs.cell_series_bytes >= cs.n_cells * 50 * n_inst * 64
+    assert sdas.results_layout(P, sdas.GridView(p, g)).cell_series_bytes == 0
+
+
+def test_step_cost_validation():
+    # worst-case RECV (h + 65535 beta + the EXP tail of alpha + KV penalty) must stay below 2^31 ticks
+    p = W.tool1(100000, svc="exp")
+    p["roles"][0]["cost"]["alpha"] = 100_000_000          # EXP tail ~22.2 x alpha > 2^31
+    with pytest.raises(sdas.SdasError) as e:
+        sdas.Pipeline(p)
+    assert e.value.code == sdas.E_INVALID_FIELD
+    p["roles"][0]["cost"]["alpha"] = 90_000_000           # 22.2 x 9e7 = 2.0e9 < 2^31
+    sdas.Pipeline(p)
+    p = W.p2_kv(ctx_tokens=40000)
+    p["roles"][1]["cost"]["beta"] = 30000                 # RECOMPUTE penalty 1.2e9 + 65535 beta > 2^31
+    with pytest.raises(sdas.SdasError):
+        sdas.Pipeline(p)
