@@ -593,8 +593,9 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
           }
         }
       }
-      if (role == ((modes >> 28) & 7u)) {  // first output token at a feedback-role instance (M13)
-        // (two items of one request may both reach done == 1 in this step: the CAS lets the first set it)
+      if (!LAZY && role == ((modes >> 28) & 7u)) {  // first output token at a feedback-role instance (M13)
+        // (two items of one request may both reach done == 1 in this step: the CAS lets the first set it;
+        // LAZY runs recorded it when the run started)
         if (act && done == 1u) atomicCAS(&rFF[slot], kUnsetFF, t - rA[slot]);
         __syncwarp();
       }
@@ -803,7 +804,9 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
           bat[64 + lane] = 0xFF000000u;
           if (MAXOUT > 1) { bat[96 + lane] = wD; bat[128 + lane] = 0xFF00u; }
         }
-        __syncwarp();
+        // every lane reads back only its own batch words; the two-level refill below rewrites wait slots
+        // other lanes have just read
+        if (SPILL) __syncwarp();
         const uint32_t pmw = min(I.wait_cap, RS);
         if (SPILL && wn_i > pmw) {   // refill the vacated slots with the oldest extension entries
           const uint32_t m = min(nadm, wn_i - pmw), g0 = H->gh[2][i], cx = I.wait_cap - RS;
