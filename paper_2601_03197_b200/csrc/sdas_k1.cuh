@@ -1092,6 +1092,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
       if (!final_partial) snap = fn + in + (st == RECV ? 1u : 0u) + wn + b;   // M31: the controller's poll
       __syncwarp();
       if (lane == 0) { H->w_n = 0; H->w_good = 0; H->w_half = 0; }
+      __syncwarp();                        // the next window's control (same event) reads them
     };
 
     // lane-local DELIVER: move the in-flight head messages due by now (strict: due before now) into the
