@@ -22,6 +22,12 @@ Pins (tests/test_oracle_*.py), each independent of the oracle's own code:
   * Statistics: M/D/1 and M/M/1 mean waits (Pollaczek-Khinchine), M/G/1.
   * Little's law (integral N_sys dt == sum e2e) and message/token conservation.
   * Controller: HT-4 table; JSQ: HT-5; bins/percentiles: HT-7 + brute force.
+  * Round 2 (tests/test_oracle_control.py, test_oracle_argmin.py, test_oracle_cellseries.py):
+    hand-derived sequences for SLO batch control M16(ii), model selection M16(iii), RR and
+    route overrides M11, the LOAD metric, max_ticks truncation, overflow ticks (R-OVF) and
+    saturated latencies (R-SAT); every argmin objective per group and per pooled row against a
+    tuple-key brute force (R-KEYS, R-RATE0); the cell-summed series (R-CSER).  Each of 28
+    plausible slips in oracle.cpp turns one of them red (tools/mutate_oracle.py).
 Parity unpinned: the full LLM-agent model (batching + RECV-first + modes) at scale
 has no closed form; it is pinned only compositionally (DESIGN.md §"Parity pins").
 """

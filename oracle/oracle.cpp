@@ -17,7 +17,10 @@
 //
 // Parity unpinned: the full model at scale (batching + RECV-first + modes +
 // control) has no closed form; it is pinned compositionally by the hand traces, queueing
-// closed forms, conservation laws and brute-force checks under tests/test_oracle_*.py.
+// closed forms, conservation laws and brute-force checks under tests/test_oracle_*.py.  Every
+// decision rule configs 3-5 rank by (M16(ii)/(iii), M11 RR, LOAD metric, truncation, R-OVF,
+// R-SAT, M20 argmins, M15 cell series) has its own hand-derived or brute-force pin
+// (tests/test_oracle_control.py, test_oracle_argmin.py, test_oracle_cellseries.py).
 //
 // Deliberately naive: std::priority_queue of events, std::deque queues,
 // std::vector<Item> batches, std::sort for percentiles.  No code is shared with
