@@ -437,7 +437,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
       }
       __syncwarp();                        // lane 0's ring writes precede the destinations' DELIVER reads
       // first feedback = the earliest first-output tick of the request's items (M13); a DECODE item may have
-      // recorded a later one in advance (LAZY), so take the minimum
+      // recorded a later one in advance (coalesced runs), so take the minimum
       if (lane == 0 && role == ((modes >> 28) & 7u)) rFF[slot] = min(rFF[slot], t - rA[slot]);
       if (P.inst[i].flags & 1u) { if (lane == (int)i) ++n_large; }
       item_done(slot);
@@ -593,9 +593,9 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
           }
         }
       }
-      if (!LAZY && role == ((modes >> 28) & 7u)) {  // first output token at a feedback-role instance (M13)
+      if (!coalesce && role == ((modes >> 28) & 7u)) {  // first output token at a feedback-role instance (M13)
         // (two items of one request may both reach done == 1 in this step: the CAS lets the first set it;
-        // LAZY runs recorded it when the run started)
+        // coalesced runs recorded it when the run started)
         if (act && done == 1u) atomicCAS(&rFF[slot], kUnsetFF, t - rA[slot]);
         __syncwarp();
       }
@@ -841,12 +841,12 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
           uint32_t lim = wA >> 16;                                      // out
           if (n_out > 0 && !ahead) lim = min(lim, wB >> 16);
           if (MAXOUT > 1 && n_out > 1) lim = min(lim, wD & 0xFFFFu);
-          // LAZY: a sequence's first token lands at the end of this run's first step, known now, so the
+          // a sequence's first token lands at the end of this run's first step, known now, so the
           // first feedback (M13: the earliest such tick of the request) is recorded now and is no stop
           // point; rFF is read only when the request completes, after every one of its items finished
           const bool first = role == ((modes >> 28) & 7u) && done == 0u;
-          if (LAZY && first) atomicMin(&rFF[wA & 0xFFFu], t + cost32 - rA[wA & 0xFFFu]);
-          sk = (!LAZY && first) ? 1u : lim - done;
+          if (first) atomicMin(&rFF[wA & 0xFFFu], t + cost32 - rA[wA & 0xFFFu]);
+          sk = lim - done;
         }
         m = __reduce_min_sync(FULL, sk);
         if (m > 1) {
