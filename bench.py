@@ -218,10 +218,19 @@ def main():
 
     rank, world, local = env_rank()
     assert world == args.gpus, "launch N>1 under torch.distributed.run with --nproc-per-node N"
+    # SDAS_BENCH_BACKEND=gloo: test hook only (tests/test_gpu_bench_multirank.py) -- several ranks share the
+    # box's GPU(s) with host-staged collectives, to exercise the N > 1 code path on a one-GPU box; the driver's
+    # runs use NCCL, one rank per GPU
+    backend = os.environ.get("SDAS_BENCH_BACKEND", "nccl")
+    if backend != "nccl":
+        local %= torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     pipe, grid = workload(args, world)
     P = sdas.Pipeline(pipe)
     S_total = grid["n_seeds"]
@@ -288,10 +297,13 @@ def main():
     k3_ms = [e[1].elapsed_time(e[2]) for e in evs]
     coll_ms = [e[3].elapsed_time(e[4]) for e in evs]
     fin_ms = [e[4].elapsed_time(e[5]) for e in evs]
-    local_ms = torch.tensor([sum(step_ms)], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(local_ms, op=dist.ReduceOp.MAX)
-    total_ms = float(local_ms.item())
+    def max_over_ranks(v):                                             # device time, max over ranks
+        x = torch.tensor([v], dtype=torch.float64, device=dev if backend == "nccl" else "cpu")
+        if world > 1:
+            dist.all_reduce(x, op=dist.ReduceOp.MAX)
+        return float(x.item())
+
+    total_ms = max_over_ranks(sum(step_ms))
     loc = acc_local.cpu().numpy()
     glob = acc_global.cpu().numpy()
     if world == 1:
@@ -359,11 +371,8 @@ def main():
             b.synchronize()
             e2e_ms.append(a.elapsed_time(b))
             h2d = L.params_bytes
-        t = torch.tensor([sum(e2e_ms)], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
         d2h = sum(h.numel() for h in pinned.values())
-        e2e = {"value": msg / (float(t.item()) / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+        e2e = {"value": msg / (max_over_ranks(sum(e2e_ms)) / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h)}
 
     flush_leg = None
@@ -405,9 +414,11 @@ def main():
             "config": {"workload": workload_name(args),
                        "replicas_per_step": reps // args.steps, "n_requests": args.requests,
                        "l2": "flushed (256 MiB write) before every step",
-                       "parallelism": "replica-grid dp%d (group-interleaved), NCCL all_reduce of cells" % world},
+                       "parallelism": "replica-grid dp%d (group-interleaved), %s all_reduce of cells" % (
+                           world, "NCCL" if backend == "nccl" else backend)},
             "replicas_per_s": reps / (total_ms / 1e3),
             "des_events_per_s": des / (total_ms / 1e3),
+            "events_per_step": {"message": msg // args.steps, "des": des // args.steps},
             "phase_ms": {"k1_simulate": statistics.mean(k1_ms), "k3_group_argmin": statistics.mean(k3_ms),
                          "collective": statistics.mean(coll_ms), "k4k5_finalize": statistics.mean(fin_ms)},
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "warp-instr/s x1e12",
