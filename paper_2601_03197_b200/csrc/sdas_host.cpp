@@ -366,6 +366,10 @@ sdas_status plan(const sdas_pipeline* p, const sdas_grid* g, Plan& pl) {
     h.off_reqCls = (uint32_t)o; o += h.cls ? R : 0;         // u8 class per request slot (M26)
     o = align_up(o, 16);
     h.off_bitmap = (uint32_t)o; o += 4ull * h.bitmap_words;
+    if (h.lean == 2) {                                      // LEAN: arrival draw queue
+      o = align_up(o, 16);
+      h.off_arrq = (uint32_t)o; o += 32ull * 8 + 32ull * 4;
+    }
     uint64_t gx = 0;
     for (uint32_t i = 0; i < h.n_inst; ++i) {
       DInst& I = h.inst[i];

@@ -68,7 +68,8 @@ struct alignas(16) DParams {
   uint32_t max_out, need_lint, kv_role, kv_ctx, kv_tau, off_reqHome;
   uint32_t cls, off_reqCls;   // f2: two request classes (class-1 rings follow the class-0 rings)
   uint32_t need_pace, lean;   // f4: some link or candidate paces (M30); lean: K1 specialisation (§5.3)
-  uint32_t ring_s, pad_rs;    // shared-memory ring size bound (levels >= 1; 0xFFFFFFFF = every ring whole)
+  uint32_t ring_s;            // shared-memory ring size bound (levels >= 1; 0xFFFFFFFF = every ring whole)
+  uint32_t off_arrq;          // LEAN: per-warp queue of the next 32 Poisson arrivals' draws (32 x u64 gap, 32 x u32 P|O)
   uint64_t off_gx, gx_per_warp;   // ring extension areas in `work`: warp w's at off_gx + w * gx_per_warp
   uint64_t off_rec_cls;       // f2: byte offset in `work` of the per-warp record-class arrays
   uint64_t kv_skew32;         // M21: home = instance 0 iff ATTR.w2 < kv_skew32 = floor(skew * 2^32 / 1000)

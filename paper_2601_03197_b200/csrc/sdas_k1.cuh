@@ -220,6 +220,29 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
     // ---------------------------------------------------------------- arrivals (M4, M5)
     auto gen = [&](uint32_t j, unsigned long long A_prev) {
       const uint32_t kind = ad.kind;
+      if (LEAN && kind == SDAS_POISSON) {
+        // the draws of arrival j (M4 gap, M5 P and O) depend on j only: every 32nd arrival, lane k draws
+        // those of arrival j + k in parallel into a per-warp queue, so 31 of 32 arrivals cost two loads
+        // instead of two Philox chains on the event loop's critical path
+        unsigned long long* const gq = reinterpret_cast<unsigned long long*>(Wr + Pk.off_arrq);
+        uint32_t* const pq = reinterpret_cast<uint32_t*>(Wr + Pk.off_arrq + 256u);
+        if ((j & 31u) == 0u) {
+          const uint32_t jj = j + (uint32_t)lane;
+          const uint2 w = philox(jj, s_coord, 1u << 16, 0u, key0, key1);
+          const uint4 v = philox4(jj, s_coord, 2u << 16, 0u, key0, key1);
+          __syncwarp();                                    // the previous block's last reads are done
+          gq[lane] = exp_sample(ad.gap0, w.x);
+          pq[lane] = uni(ad.p_lo, ad.p_hi, v.x) | (uni(ad.o_lo, ad.o_hi, v.y) << 16);   // both <= 65535
+          __syncwarp();
+        }
+        A_next = A_prev + gq[j & 31u];
+        const uint32_t po = pq[j & 31u];
+        P_next = po & 0xFFFFu;
+        O_next = po >> 16;
+        arr_near = A_next - t < 0x80000000ull;
+        A_lo = (uint32_t)A_next;
+        return;
+      }
       if (kind == SDAS_POISSON) {
         const uint2 w = philox(j, s_coord, 1u << 16, 0u, key0, key1);
         A_next = A_prev + exp_sample(ad.gap0, w.x);
