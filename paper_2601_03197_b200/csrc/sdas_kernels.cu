@@ -333,6 +333,9 @@ typedef void (*K1Fn)(const uint8_t*, Work*, uint8_t*, unsigned long long*, uint8
                      unsigned long long*, DParams);
 
 static K1Fn k1_pick(bool trace, uint32_t maxout, bool cls, uint32_t lv, bool spill) {
+#ifdef K1_EXP_LEAN_ONLY   // register / SASS experiments only: compile the config-2 instantiation alone
+  return k1_simulate<false, 1, false, 2, false>;
+#else
   if (!trace && !cls && lv == 2 && maxout == 1)
     return spill ? k1_simulate<false, 1, false, 2, true> : k1_simulate<false, 1, false, 2, false>;
   if (!trace && !cls && lv >= 1) {
@@ -345,6 +348,7 @@ static K1Fn k1_pick(bool trace, uint32_t maxout, bool cls, uint32_t lv, bool spi
   }
   if (maxout > 1) return trace ? k1_simulate<true, 2, false, 0, false> : k1_simulate<false, 2, false, 0, false>;
   return trace ? k1_simulate<true, 1, false, 0, false> : k1_simulate<false, 1, false, 0, false>;
+#endif
 }
 
 int launch_simulate(const uint8_t* params_dev, const DParams& hp, const sdas_buffers* bf, uint32_t blocks,
