@@ -295,6 +295,11 @@ sdas_status plan(const sdas_pipeline* p, const sdas_grid* g, Plan& pl) {
     }
     inst += R.n_instances;
   }
+  auto rcp32 = [](uint64_t d) -> uint32_t { return d <= 1 ? 0xFFFFFFFFu : (uint32_t)((1ull << 32) / d); };
+  for (uint32_t i = 0; i < h.n_inst; ++i)
+    for (uint32_t b = 0; b <= SDAS_MAX_BATCH; ++b)
+      h.rcp_step[i][b] = rcp32(std::max<uint64_t>(1, (uint64_t)h.inst[i].tau0 + (uint64_t)h.inst[i].gamma * b));
+  for (uint32_t f = 0; f < 256; ++f) h.rcp_fn[f] = rcp32(f);
   for (uint32_t l = 0; l < nl; ++l) {
     const sdas_link_desc& L = p->links[l];
     DLink& D = h.link[l];

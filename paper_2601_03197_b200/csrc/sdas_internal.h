@@ -79,6 +79,11 @@ struct alignas(16) DParams {
   DInst inst[SDAS_MAX_INSTANCES];
   DRole role[SDAS_MAX_ROLES];
   DLink link[SDAS_MAX_LINKS + 1];
+  // reciprocals for K1's divisions (a u32 division by a variable is a ~125-cycle dependent chain on B200):
+  // rcp_step[i][b] = floor(2^32 / c) for instance i's DECODE step cost c = max(1, tau0 + gamma b) (M7),
+  // rcp_fn[f] = floor(2^32 / f) for FUNCTION emission-point divisors f = 1..255 (M9); 0xFFFFFFFF for 1
+  uint32_t rcp_step[SDAS_MAX_INSTANCES][SDAS_MAX_BATCH + 1];
+  uint32_t rcp_fn[256];
 };
 
 static_assert(sizeof(DInst) == 80, "DInst");

@@ -163,7 +163,9 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
     // nothing any other part of the model observes, so they complete as one event at end_lo with the
     // per-step bookkeeping applied in bulk.  A message or arrival entering the inbox mid-run cuts the run
     // at the first step boundary >= its tick (RECV-first START, M7); flushm > 0 = a cut landed exactly
-    // on a boundary of this tick and that many silent steps are applied before phase START.
+    // on a boundary of this tick: that many silent steps end now (the instance is idle for START) and the
+    // batch words still lack them -- the instance's next start_decode adds them (TRACE builds: the flush
+    // loop before START applies them, with their trace records).
     uint32_t runm = 1, flushm = 0;
     // f2: class-1 (interactive) ring heads and counts; `in` / `wn` stay the totals over both rings
     uint32_t ih1 = 0, in1 = 0, wh1 = 0, wn1 = 0;
@@ -303,7 +305,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
       if (st != DECODE || runm <= 1u) return;
       const uint32_t c = max(1u, MI.tau0 + MI.gamma * b);
       const uint32_t rs = end_lo - runm * c;
-      const uint32_t mp = (x - rs + c - 1u) / c;
+      const uint32_t mp = div_rcp(x - rs + c - 1u, c, P.rcp_step[lane][b]);
       if (mp < runm) {
         runm = mp;
         end_lo = rs + mp * c;
@@ -521,7 +523,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
             if (mode == SDAS_FUNCTION) {
               ++fidx;
               const uint32_t Fp = min(R.n_functions, out);
-              nx = ((fidx + 1u) * out) / Fp   /* < 2^24: fidx < 256, out < 2^16 */;
+              nx = div_rcp((fidx + 1u) * out, Fp, P.rcp_fn[Fp])   /* < 2^24: fidx < 256, out < 2^16 */;
             } else if (tm) {
               nx = min(next + P.link[l].chunk, out);
             }
@@ -764,7 +766,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
           prev = nxt;
           if (mode == SDAS_FUNCTION) {
             ++fidx;
-            nxt = ((fidx + 1u) * out) / Fp   /* < 2^24: fidx < 256, out < 2^16 */;
+            nxt = div_rcp((fidx + 1u) * out, Fp, P.rcp_fn[Fp])   /* < 2^24: fidx < 256, out < 2^16 */;
           } else {                                          // TOKEN (BATCH emits at the end only)
             nxt = min(nxt + chunk, out);
           }
@@ -816,7 +818,10 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
             const uint32_t l = q ? R.out_link1 : R.out_link0;
             const uint32_t mode = (modes >> (2 * l)) & 3u;
             uint32_t next = out;
-            if (mode == SDAS_FUNCTION) next = out / min(R.n_functions, out);
+            if (mode == SDAS_FUNCTION) {
+              const uint32_t Fp = min(R.n_functions, out);   // >= 1: batch items have out >= 1
+              next = div_rcp(out, Fp, P.rcp_fn[Fp]);
+            }
             else if (mode == SDAS_TOKEN) next = min(P.link[l].chunk, out);
             wA |= mode << (12 + 2 * q);
             if (q == 0) wB = next << 16;
@@ -844,6 +849,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
       // branch-free update of instance i (tau0 < 2^31 and gamma*32 < 2^30 are validated: no u32 overflow)
       const bool me = lane == (int)i;
       const uint32_t cost32 = max(1u, I.tau0 + I.gamma * nbat);
+      const uint32_t rc = P.rcp_step[i][nbat];           // floor(2^32 / cost32), for the run-length divisions
       // run length: steps until the first sequence reaches an emission point / its end / first feedback.
       // AHEAD: the source role's inbox receives arrivals only, so its run is known up to the
       // next arrival; its emission points do not end the run -- their messages are emitted now, each with
@@ -858,6 +864,13 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
           wA = bat[lane];
           wB = bat[32 + lane];
           if (MAXOUT > 1) wD = bat[96 + lane];
+        }
+        if (!TRACE) {                      // silent steps of a run cut exactly at a boundary (cut_run)
+          const uint32_t fl = __shfl_sync(FULL, flushm, i);
+          if (fl) {
+            if (lane < (int)bi) bat[32 + lane] = wB += fl;   // done += fl (stays below every stop point)
+            flushm = lane == (int)i ? 0u : flushm;
+          }
         }
         if (lane < (int)nbat) {
           const uint32_t done = wB & 0xFFFFu;
@@ -875,19 +888,19 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
         if (m > 1) {
           // keep every pending tick < 2^31 ahead; end at the first boundary >= the next window when the
           // controller could change B while items wait; never step past max_ticks
-          if ((unsigned long long)m * cost32 >= (1ull << 30)) m = max(1u, (1u << 30) / cost32);
+          if ((unsigned long long)m * cost32 >= (1ull << 30)) m = max(1u, div_rcp(1u << 30, cost32, rc));
           if (LAZY) {                                      // end at the first boundary >= a pending delivery
             const uint32_t fn_i = __shfl_sync(FULL, fn, i), fh_i = __shfl_sync(FULL, fhead, i);
-            if (fn_i) m = min(m, max(1u, (fh_i - t_lo + cost32 - 1u) / cost32));
+            if (fn_i) m = min(m, max(1u, div_rcp(fh_i - t_lo + cost32 - 1u, cost32, rc)));
           }
           const uint32_t span = m * cost32;
           if ((modes >> 31) && wn_i > nadm) {
             const uint32_t nbd = nb_lo - t_lo;
-            if (span > nbd) m = (nbd + cost32 - 1u) / cost32;
+            if (span > nbd) m = div_rcp(nbd + cost32 - 1u, cost32, rc);
           }
           if (max_ticks && t + span > max_ticks)
             m = (uint32_t)max(1ull, (max_ticks - min(t, max_ticks)) / cost32);
-          if (ahead && arr_near) m = min(m, max(1u, (A_lo - t_lo + cost32 - 1u) / cost32));   // next arrival
+          if (ahead && arr_near) m = min(m, max(1u, div_rcp(A_lo - t_lo + cost32 - 1u, cost32, rc)));   // next arrival
         }
         if (ahead && m > 1) m = emit_ahead(i, R, nbat, cost32, m, wA, wB);
       }
@@ -909,15 +922,20 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
       if (st != DECODE || runm <= 1u) return;
       const uint32_t c = max(1u, MI.tau0 + MI.gamma * b);
       const uint32_t rs = end_lo - runm * c;                 // run start (>= 1 tick ago)
-      const uint32_t mp = (t_lo - rs + c - 1u) / c;          // first boundary >= t
+      const uint32_t mp = div_rcp(t_lo - rs + c - 1u, c, P.rcp_step[lane][b]);   // first boundary >= t
       if (mp >= runm) return;
       if (rs + mp * c != t_lo) {
         runm = mp;
         end_lo = rs + mp * c;
-      } else {                                               // boundary at this very tick: flush it
+      } else if (TRACE) {                                    // boundary at this very tick: flush it
         flushm = mp;
         runm = mp;
         end_lo = t_lo;
+      } else {                                               // boundary at this very tick: the run ends
+        st = IDLE;
+        cnt_decode += mp;
+        tok += (unsigned long long)mp * b;
+        flushm = mp;                                         // done += mp: at the next start_decode
       }
     };
 
@@ -1278,7 +1296,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
         if (K1_UNLIKELY(ovf)) break;
       }
       // runs cut exactly at this tick: apply their silent steps (they precede START, as in M12)
-      if (coalesce && cut) {
+      if (TRACE && coalesce && cut) {
         uint32_t fm = __ballot_sync(FULL, flushm != 0u);
         while (fm) {
           const int i = __ffs(fm) - 1;
@@ -1419,22 +1437,28 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
       }
       val = lo + prefix;
     };
-    uint32_t v50e = 0xFFFFFFFFu, v99e = 0xFFFFFFFFu, v50f = 0xFFFFFFFFu, v99f = 0xFFFFFFFFu, v90e = 0xFFFFFFFFu;
-    uint32_t b50e = 0xFFFFu, b99e = 0xFFFFu, b50f = 0xFFFFu, b99f = 0xFFFFu, b90e = 0xFFFFu;
-    if (completed > 0) {
-      const uint32_t k50 = (uint32_t)((50ull * completed + 99ull) / 100ull);
-      const uint32_t k99 = (uint32_t)((99ull * completed + 99ull) / 100ull);
-      select(he, 0, k50, v50e, b50e, false);
-      select(he, 0, k99, v99e, b99e, false);
-      select(he, 0, (uint32_t)((90ull * completed + 99ull) / 100ull), v90e, b90e, false);
-      select(hf, 1, k50, v50f, b50f, false);
-      select(hf, 1, k99, v99f, b99f, false);
-    }
-    uint32_t v50i = 0xFFFFFFFFu, v99i = 0xFFFFFFFFu, bi_unused = 0;
+    // one select per quantile in a rolled loop: five (seven) inlined copies of the radix select evicted the
+    // event loop from the instruction cache whenever a warp finalized.  q = 0..4: e2e p50,
+    // p99, p90, first-feedback p50, p99; CLS q = 5, 6: interactive e2e p50, p99 (M29).  Each result goes
+    // straight to its summary word (bins as u16 halves of words 16 and 41); empty sets keep the sentinels.
     const uint32_t n_int = CLS ? H->completed_int : 0u;
-    if (CLS && n_int > 0) {             // M29: exact percentiles over the interactive records alone
-      select(hi, 0, (uint32_t)((50ull * n_int + 99ull) / 100ull), v50i, bi_unused, true);
-      select(hi, 0, (uint32_t)((99ull * n_int + 99ull) / 100ull), v99i, bi_unused, true);
+    if (lane == 0) {
+      stg[12] = stg[13] = stg[14] = stg[15] = stg[16] = stg[17] = stg[41] = 0xFFFFFFFFu;
+      stg[36] = stg[37] = 0xFFFFFFFFu;
+    }
+    __syncwarp();
+    const uint32_t nq = completed == 0 ? 0u : (CLS && n_int > 0) ? 7u : 5u;
+#pragma unroll 1
+    for (uint32_t q = 0; q < nq; ++q) {
+      const bool fq = q == 3 || q == 4, iq = q >= 5;
+      const uint32_t pc = (q == 0 || q == 3 || q == 5) ? 50u : q == 2 ? 90u : 99u;
+      const uint32_t kq = (uint32_t)((pc * (unsigned long long)(iq ? n_int : completed) + 99ull) / 100ull);
+      uint32_t v = 0, bq = 0;
+      select(iq ? hi : fq ? hf : he, fq ? 1 : 0, kq, v, bq, iq);
+      if (lane == 0) {
+        stg[q == 0 ? 12 : q == 1 ? 13 : q == 2 ? 17 : q == 3 ? 14 : q == 4 ? 15 : q == 5 ? 36 : 37] = v;
+        if (q != 2 && q < 5) reinterpret_cast<uint16_t*>(stg)[q == 0 ? 32 : q == 1 ? 33 : q == 3 ? 82 : 83] = (uint16_t)bq;
+      }
     }
     const uint32_t deliv = __reduce_add_sync(FULL, is_inst ? cnt_deliv : 0u);
     const uint32_t recvs = __reduce_add_sync(FULL, is_inst ? cnt_recv : 0u);
@@ -1455,8 +1479,6 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
       stg[6] = (uint32_t)sum_e2e; stg[7] = (uint32_t)(sum_e2e >> 32);
       stg[8] = (uint32_t)sum_ff; stg[9] = (uint32_t)(sum_ff >> 32);
       stg[10] = (uint32_t)int_nsys; stg[11] = (uint32_t)(int_nsys >> 32);
-      stg[12] = v50e; stg[13] = v99e; stg[14] = v50f; stg[15] = v99f;
-      stg[16] = b50e | (b99e << 16); stg[17] = v90e;
       stg[18] = h.max_e2e; stg[19] = n_sat;
       stg[20] = arrivals; stg[21] = deliv; stg[22] = recvs; stg[23] = decs;
       stg[24] = window_closes; stg[25] = mode_switches; stg[26] = good; stg[27] = larges;
@@ -1465,8 +1487,8 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
       stg[31] = kvs;
       stg[32] = h.completed_int; stg[33] = h.rejected;
       stg[34] = (uint32_t)h.sum_e2e_int; stg[35] = (uint32_t)(h.sum_e2e_int >> 32);
-      stg[36] = v50i; stg[37] = v99i; stg[38] = h.good_int; stg[39] = h.gate_changes;
-      stg[40] = select_changes; stg[41] = b50f | (b99f << 16); stg[42] = 0; stg[43] = 0;
+      stg[38] = h.good_int; stg[39] = h.gate_changes;
+      stg[40] = select_changes; stg[42] = 0; stg[43] = 0;
 #ifdef K1_COUNT_ITERS
       stg[42] = n_iter;
 #endif

@@ -103,6 +103,14 @@ __device__ __forceinline__ uint32_t bin_lo(uint32_t b) {
   return b < 16u ? b : ((16u + ((b - 16u) & 15u)) << ((b - 16u) >> 4));
 }
 
+// floor(n / d) for d >= 1 from M = floor(2^32 / d) (0xFFFFFFFF for d = 1, DParams.rcp_*): umulhi(n, M) is
+// the quotient or one less (n M > n 2^32 / d - n), so one remainder test corrects it.  Four dependent integer
+// instructions instead of the ~125-cycle division sequence.
+__device__ __forceinline__ uint32_t div_rcp(uint32_t n, uint32_t d, uint32_t M) {
+  const uint32_t q = __umulhi(n, M);
+  return n - q * d >= d ? q + 1u : q;
+}
+
 __device__ __forceinline__ uint32_t wrap_add(uint32_t a, uint32_t b, uint32_t cap) {
   const uint32_t x = a + b;
   return x >= cap ? x - cap : x;
