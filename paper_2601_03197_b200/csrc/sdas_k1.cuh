@@ -175,7 +175,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
     int32_t q_last_gate = -(1 << 30);
 
     // uniform replica state
-    unsigned long long t = 0, A_next = 0, int_nsys = 0;
+    unsigned long long t = 0, A_next = 0, int_nsys_acc = 0;
     uint32_t t_lo = 0, nb_lo = W32, A_lo = 0, jn = 0, P_next = 0, O_next = 0, nsys = 0, wk = 0;
     bool arr_near = false, ovf = false, arr_more = N > 0;
     uint32_t status = SDAS_REPLICA_OK;
@@ -1175,7 +1175,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
           H->gh[1][lane] = (uint16_t)wrap_add(g0, 1u, MI.flight_cap - RS);
         }
         --fn;
-        ++cnt_deliv;
+        if (!LV) ++cnt_deliv;   // levels >= 1: derived at the finalize
         if (TRACE) trace_lane(TR_DELIVER, lane, rJ[body & 0xFFFFu], (uint32_t)(body >> 32) & 0xFFFFu);
         if (fn == 0) return false;
         fhead = ft[fh];
@@ -1213,7 +1213,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
         acc_qint += (unsigned long long)Q * dd;
         if (dd) acc_maxq = max(acc_maxq, Q);
         if (need_lint) acc_lint += (unsigned long long)(fn + Q + (st == RECV ? 1u : 0u) + b) * dd;
-        int_nsys += (unsigned long long)nsys * dd;
+        if (!LV) int_nsys_acc += (unsigned long long)nsys * dd;   // levels >= 1: = sum_e2e at the end (finalize)
         t += dd;
         t_lo += dd;
       };
@@ -1460,8 +1460,11 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
         if (q != 2 && q < 5) reinterpret_cast<uint16_t*>(stg)[q == 0 ? 32 : q == 1 ? 33 : q == 3 ? 82 : 83] = (uint16_t)bq;
       }
     }
-    const uint32_t deliv = __reduce_add_sync(FULL, is_inst ? cnt_deliv : 0u);
     const uint32_t recvs = __reduce_add_sync(FULL, is_inst ? cnt_recv : 0u);
+    // every delivered message is received before the last request completes and every other RECV is an
+    // admitted arrival's (M7, M14): on levels >= 1 (no truncation; overflowed replicas report zeros)
+    // deliveries = RECVs - admitted
+    const uint32_t deliv = LV ? recvs - H->admitted : __reduce_add_sync(FULL, is_inst ? cnt_deliv : 0u);
     const uint32_t decs = __reduce_add_sync(FULL, is_inst ? cnt_decode : 0u);
     const uint32_t kvs = __reduce_add_sync(FULL, is_inst ? cnt_kv : 0u);
     const uint32_t larges = __reduce_add_sync(FULL, is_inst ? n_large : 0u);
@@ -1471,6 +1474,9 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
       const WarpHdr& h = *H;
       const uint32_t admitted = h.admitted, dropped = h.dropped, good = h.good, n_sat = h.n_sat;
       const unsigned long long sum_e2e = h.sum_e2e, sum_ff = h.sum_ff;
+      // integral of N(t) (M15) = sum over requests of (departure - arrival): on levels >= 1 a replica that
+      // reaches the finalize has completed every admitted request (no truncation), so it is sum_e2e
+      const unsigned long long int_nsys = LV ? sum_e2e : int_nsys_acc;
       const uint32_t window_closes = h.window_closes, mode_switches = h.mode_switches;
       const uint32_t batch_changes = h.batch_changes, select_changes = h.select_changes;
       const uint32_t arrivals = admitted + dropped;
