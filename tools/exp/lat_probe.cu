@@ -3,7 +3,8 @@
 #include <cstdio>
 #include <cstdint>
 #define N 1024
-__global__ void k(uint32_t* out, uint32_t seed, long long* cyc) {
+struct Tab { uint32_t v[1024]; };
+__global__ void k(uint32_t* out, uint32_t seed, long long* cyc, const __grid_constant__ Tab tab) {
   __shared__ uint32_t sm[1024];
   const int lane = threadIdx.x;
   for (int i = lane; i < 1024; i += 32) sm[i] = (i * 7 + 3) & 1023;
@@ -24,15 +25,20 @@ __global__ void k(uint32_t* out, uint32_t seed, long long* cyc) {
   RUN(7, v = __popc(__ballot_sync(0xffffffffu, v & 1u)) + v)          // ballot + popc
   RUN(8, if (v & 1u) v += 3u; else v ^= 5u; __syncwarp())             // uniform-ish branch + syncwarp
   RUN(9, if (lane == (int)(v & 31u)) v += 7u; v = __shfl_sync(0xffffffffu, v, 0))   // lane-0 block + shfl
+  { uint32_t u = __shfl_sync(0xffffffffu, v, 0);                      // warp-uniform index chain
+    RUN(10, u = tab.v[u & 1023u] + 1u)                                // LDC (param space, uniform index)
+    RUN(11, u = sm[u & 1023u] + 1u)                                   // LDS (uniform address)
+    v += u; }
   out[lane] = v + acc;
 }
 int main() {
   uint32_t* o; long long* c; cudaMalloc(&o, 128); cudaMalloc(&c, 8 * 16);
-  k<<<1, 32>>>(o, 1, c); cudaDeviceSynchronize();
-  k<<<1, 32>>>(o, 1, c); cudaDeviceSynchronize();
+  static Tab tab; for (int i = 0; i < 1024; ++i) tab.v[i] = (i * 7 + 3) & 1023;
+  k<<<1, 32>>>(o, 1, c, tab); cudaDeviceSynchronize();
+  k<<<1, 32>>>(o, 1, c, tab); cudaDeviceSynchronize();
   long long h[16]; cudaMemcpy(h, c, 8 * 16, cudaMemcpyDeviceToHost);
   const char* nm[] = {"IMAD+loop", "SHFL.IDX", "ballot", "REDUX.MIN", "LDS", "udiv", "any", "ballot+popc",
-                      "branch+syncwarp", "lane-if+shfl"};
-  for (int i = 0; i < 10; ++i) printf("%-16s %6.1f cyc/iter\n", nm[i], (double)h[i] / N);
+                      "branch+syncwarp", "lane-if+shfl", "LDC uniform", "LDS uniform"};
+  for (int i = 0; i < 12; ++i) printf("%-16s %6.1f cyc/iter\n", nm[i], (double)h[i] / N);
   return 0;
 }
