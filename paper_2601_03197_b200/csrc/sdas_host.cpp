@@ -371,7 +371,7 @@ sdas_status plan(const sdas_pipeline* p, const sdas_grid* g, Plan& pl) {
     h.off_reqCls = (uint32_t)o; o += h.cls ? R : 0;         // u8 class per request slot (M26)
     o = align_up(o, 16);
     h.off_bitmap = (uint32_t)o; o += 4ull * h.bitmap_words;
-    if (h.lean == 2) {                                      // LEAN: arrival draw queue
+    if (h.lean >= 1) {                                      // levels >= 1: arrival draw queue
       o = align_up(o, 16);
       h.off_arrq = (uint32_t)o; o += 32ull * 8 + 32ull * 4;
     }

@@ -222,7 +222,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
     // ---------------------------------------------------------------- arrivals (M4, M5)
     auto gen = [&](uint32_t j, unsigned long long A_prev) {
       const uint32_t kind = ad.kind;
-      if (LEAN && kind == SDAS_POISSON) {
+      if (LV >= 1 && kind == SDAS_POISSON) {   // (levels >= 1: no KV home or class draws per arrival)
         // the draws of arrival j (M4 gap, M5 P and O) depend on j only: every 32nd arrival, lane k draws
         // those of arrival j + k in parallel into a per-warp queue, so 31 of 32 arrivals cost two loads
         // instead of two Philox chains on the event loop's critical path
