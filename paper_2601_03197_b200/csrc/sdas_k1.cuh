@@ -82,6 +82,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
   // (LEAN only: on level 1 the extra code pushed the hot loop out of the instruction cache, +45 % at config 3)
   constexpr bool LAZY = LV == 2;   // deliveries into a busy instance are not events
   constexpr bool SILENT = LV == 2; // a RECV whose end changes nothing else is not an event
+  constexpr bool CHAIN = LV == 2;  // a non-closing RECV while a batch is held flows into its next run (§5.8)
   constexpr bool SPILL = SPL;                          // a separate instantiation: grids whose rings fit whole
   static_assert(!SPL || LV >= 1, "two-level rings exist on the specialised levels only");   // never pay for it
   const uint32_t RS = SPILL ? Pk.ring_s : 0xFFFFFFFFu;
@@ -301,11 +302,13 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
 
     // lane-local: a message due at tick x will enter this instance's inbox while it may be mid-run: end the
     // run at the first step boundary >= x (the cut of M7's RECV-first START, applied when x becomes known)
+    // (CHAIN, LEAN: a run may start after the current tick -- at the end of the RECV it follows; a message due
+    // before that start cuts it to 0 steps: the instance is idle at the RECV end and RECV-first takes over)
     auto cut_at = [&](uint32_t x) {
-      if (st != DECODE || runm <= 1u) return;
+      if (st != DECODE || runm <= (CHAIN ? 0u : 1u)) return;
       const uint32_t c = max(1u, MI.tau0 + MI.gamma * b);
       const uint32_t rs = end_lo - runm * c;
-      const uint32_t mp = div_rcp(x - rs + c - 1u, c, P.rcp_step[lane][b]);
+      const uint32_t mp = CHAIN && (int32_t)(x - rs) <= 0 ? 0u : div_rcp(x - rs + c - 1u, c, P.rcp_step[lane][b]);
       if (mp < runm) {
         runm = mp;
         end_lo = rs + mp * c;
@@ -659,9 +662,9 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
     };
 
     // ---------------------------------------------------------------- phase START (M7)
-    auto start_recv = [&](uint32_t i) {  // RECV-first: instance i pops its inbox head
+    auto start_recv = [&](uint32_t i) -> uint32_t {  // RECV-first: instance i pops its inbox head
       __syncwarp();                       // rNit / rJ written by other lanes earlier in this tick
-      uint32_t cost32 = 0, slot = 0;
+      uint32_t cost32 = 0, slot = 0, toff = 0;
       if (lane == (int)i) {
         const bool from1 = CLS && in1 != 0u;                  // M27: interactive messages first
         const unsigned long long body =
@@ -711,10 +714,30 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
         // SILENT (runm = 0 while in RECV): a non-closing message whose RECV end leaves nothing to start (no
         // inbox, wait or batch, no delivery due before it) only makes the instance idle: that happens at its
         // next event instead (busy is integrated up to end_lo, a delivery emitted for before end_lo re-arms it)
-        runm = (SILENT && !((body >> 17) & 1u) && in == 0u && wn == 0u && b == 0u &&
-                (fn == 0u || (int32_t)(fhead - end_lo) >= 0)) ? 0u : 1u;
+        const bool alone = SILENT && !((body >> 17) & 1u) && in == 0u;
+        runm = (alone && wn == 0u && b == 0u && (fn == 0u || (int32_t)(fhead - end_lo) >= 0)) ? 0u : 1u;
+        // CHAIN: the same message received while the instance holds a batch (RECV-first cut
+        // the batch's run): with nothing due before the RECV ends and nothing to admit then (no waiting item,
+        // or a full batch and no window close -- a possible B change -- up to the RECV end), the batch's next
+        // run starts exactly then, so start_decode computes it now from that tick and the RECV end is no event
+        // (a non-closing RECV completes with nothing but the count, M8)
+#ifdef K1_COUNT_ITERS
+        if (SILENT && !((body >> 17) & 1u) && b != 0u) {   // experiment: why a chain candidate fails
+          atomicAdd(&work->pad[16], 1ull);
+          if (in != 0u) atomicAdd(&work->pad[17], 1ull);
+          if (!(wn == 0u || (b >= Bk && (int32_t)(nb_lo - end_lo) > 0))) atomicAdd(&work->pad[18], 1ull);
+          if (!(fn == 0u || (int32_t)(fhead - end_lo) > 0)) atomicAdd(&work->pad[19], 1ull);
+          if (wn != 0u) atomicAdd(&work->pad[20], 1ull);
+        }
+#endif
+        if (CHAIN && alone && b != 0u && (wn == 0u || (b >= Bk && (int32_t)(nb_lo - end_lo) > 0)) &&
+            (fn == 0u || (int32_t)(fhead - end_lo) > 0) && cost32 < (1u << 29)) {
+          toff = cost32;
+          ++cnt_recv;
+        }
       }
       if (TRACE) trace(TR_RECV_START, i, rJ[__shfl_sync(FULL, slot, i)], __shfl_sync(FULL, cost32, i));
+      return CHAIN ? __shfl_sync(FULL, toff, i) : 0u;
     };
     // AHEAD: emit now the messages of the emission points the source instance i passes at
     // steps 1 .. m-1 of its run (step k's messages carry emission tick t + k c, in batch order, M9); the
@@ -789,7 +812,10 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
       }
       return m;
     };
-    auto start_decode = [&](uint32_t i) {  // FIFO admission (modes bound here, M9) + DECODE step / run
+    // toff > 0 (CHAIN): the run starts toff ticks from now, when the RECV started this tick ends (no admission:
+    // nothing waits)
+    auto start_decode = [&](uint32_t i, uint32_t toff) {  // FIFO admission (modes bound here, M9) + DECODE step / run
+      const uint32_t ts = t_lo + toff;                      // the run's start tick
       const DInst& I = P.inst[i];
       const uint32_t role = LEAN ? i : I.role;
       const DRole& R = P.role[role];
@@ -881,7 +907,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
           // first feedback (M13: the earliest such tick of the request) is recorded now and is no stop
           // point; rFF is read only when the request completes, after every one of its items finished
           const bool first = role == ((modes >> 28) & 7u) && done == 0u;
-          if (first) atomicMin(&rFF[wA & 0xFFFu], t + cost32 - rA[wA & 0xFFFu]);
+          if (first) atomicMin(&rFF[wA & 0xFFFu], t + toff + cost32 - rA[wA & 0xFFFu]);
           sk = lim - done;
         }
         m = __reduce_min_sync(FULL, sk);
@@ -891,16 +917,16 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
           if ((unsigned long long)m * cost32 >= (1ull << 30)) m = max(1u, div_rcp(1u << 30, cost32, rc));
           if (LAZY) {                                      // end at the first boundary >= a pending delivery
             const uint32_t fn_i = __shfl_sync(FULL, fn, i), fh_i = __shfl_sync(FULL, fhead, i);
-            if (fn_i) m = min(m, max(1u, div_rcp(fh_i - t_lo + cost32 - 1u, cost32, rc)));
+            if (fn_i) m = min(m, max(1u, div_rcp(fh_i - ts + cost32 - 1u, cost32, rc)));
           }
           const uint32_t span = m * cost32;
           if ((modes >> 31) && wn_i > nadm) {
-            const uint32_t nbd = nb_lo - t_lo;
+            const uint32_t nbd = nb_lo - ts;
             if (span > nbd) m = div_rcp(nbd + cost32 - 1u, cost32, rc);
           }
           if (max_ticks && t + span > max_ticks)
             m = (uint32_t)max(1ull, (max_ticks - min(t, max_ticks)) / cost32);
-          if (ahead && arr_near) m = min(m, max(1u, div_rcp(A_lo - t_lo + cost32 - 1u, cost32, rc)));   // next arrival
+          if (ahead && arr_near) m = min(m, max(1u, div_rcp(A_lo - ts + cost32 - 1u, cost32, rc)));   // next arrival
         }
         if (ahead && m > 1) m = emit_ahead(i, R, nbat, cost32, m, wA, wB);
       }
@@ -913,16 +939,17 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
       b = me ? nbat : b;
       const bool go = me && nbat > 0;
       st = go ? (uint32_t)DECODE : st;
-      end_lo = go ? t_lo + m * cost32 : end_lo;
+      end_lo = go ? ts + m * cost32 : end_lo;
       runm = go ? m : runm;
       if (TRACE && nbat > 0) trace(TR_DECODE_START, i, nbat, cost32);
     };
     // lane-local: a message / arrival enters this instance's inbox at tick t while it may be mid-run
     auto cut_run = [&]() {
-      if (st != DECODE || runm <= 1u) return;
+      if (st != DECODE || runm <= (CHAIN ? 0u : 1u)) return;
       const uint32_t c = max(1u, MI.tau0 + MI.gamma * b);
-      const uint32_t rs = end_lo - runm * c;                 // run start (>= 1 tick ago)
-      const uint32_t mp = div_rcp(t_lo - rs + c - 1u, c, P.rcp_step[lane][b]);   // first boundary >= t
+      const uint32_t rs = end_lo - runm * c;                 // run start (>= 1 tick ago; CHAIN: maybe ahead)
+      const uint32_t mp = CHAIN && (int32_t)(t_lo - rs) <= 0 ? 0u
+                                                             : div_rcp(t_lo - rs + c - 1u, c, P.rcp_step[lane][b]);   // first boundary >= t
       if (mp >= runm) return;
       if (rs + mp * c != t_lo) {
         runm = mp;
@@ -1328,8 +1355,10 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
         do {
           const int i = __ffs(sm) - 1;
           sm &= sm - 1;
-          if ((recvm >> i) & 1u) start_recv((uint32_t)i);
-          else start_decode((uint32_t)i);
+          const bool rv = (recvm >> i) & 1u;
+          uint32_t toff = 0;
+          if (rv) toff = start_recv((uint32_t)i);
+          if (!rv || toff) start_decode((uint32_t)i, toff);   // (one call site: the chained run included)
         } while (sm);
       }
 #ifdef K1_COUNT_ITERS

@@ -34,3 +34,6 @@ for name, fl in (("auto", 0), ("generic", sdas.FLAG_GENERIC)):
     # work words: [0] replica counter, [1 + 1 + f] = pad[1 + f] iterations with flag f, [1 + 8 + f] only flag f
     print("  iterations with flag (share):", ", ".join("%s %.3f" % (n, w[2 + f] / tot_it) for f, n in enumerate(names)))
     print("  iterations with only that flag:", ", ".join("%s %.3f" % (n, w[9 + f] / tot_it) for f, n in enumerate(names)))
+    if w[17]:   # pad[16..20]: non-closing RECVs while a batch is held (CHAIN candidates) and why one fails
+        print("  chain candidates %d: inbox not empty %d, admission possible %d, delivery due %d, items waiting %d"
+              % (w[17], w[18], w[19], w[20], w[21]))
