@@ -910,6 +910,21 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
           if (first) atomicMin(&rFF[wA & 0xFFFu], t + toff + cost32 - rA[wA & 0xFFFu]);
           sk = lim - done;
         }
+        if (LV) {
+          // every run bound is a minimum, so they are computed beside the warp-min instead of one after the
+          // other behind it: keep every pending tick < 2^31 ahead (min(m, max(1, 2^30 / c)) is the cap); end
+          // at the first boundary >= a pending delivery (LAZY), >= the next window when the controller could
+          // change B while items wait, >= the next arrival (AHEAD)
+          uint32_t bnd = max(1u, div_rcp(1u << 30, cost32, rc));
+          if (LAZY) {
+            const uint32_t fn_i = __shfl_sync(FULL, fn, i), fh_i = __shfl_sync(FULL, fhead, i);
+            if (fn_i) bnd = min(bnd, max(1u, div_rcp(fh_i - ts + cost32 - 1u, cost32, rc)));
+          }
+          if ((modes >> 31) && wn_i > nadm) bnd = min(bnd, div_rcp(nb_lo - ts + cost32 - 1u, cost32, rc));
+          if (ahead && arr_near) bnd = min(bnd, max(1u, div_rcp(A_lo - ts + cost32 - 1u, cost32, rc)));
+          m = __reduce_min_sync(FULL, sk);
+          if (m > 1) m = min(m, bnd);
+        } else {
         m = __reduce_min_sync(FULL, sk);
         if (m > 1) {
           // keep every pending tick < 2^31 ahead; end at the first boundary >= the next window when the
@@ -927,6 +942,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
           if (max_ticks && t + span > max_ticks)
             m = (uint32_t)max(1ull, (max_ticks - min(t, max_ticks)) / cost32);
           if (ahead && arr_near) m = min(m, max(1u, div_rcp(A_lo - ts + cost32 - 1u, cost32, rc)));   // next arrival
+        }
         }
         if (ahead && m > 1) m = emit_ahead(i, R, nbat, cost32, m, wA, wB);
       }
