@@ -410,6 +410,8 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
       const uint32_t role = LEAN ? i : I.role;      // LEAN: instance i is role i's only instance
       const DRole& R = P.role[role];
       const unsigned long long body = __shfl_sync(FULL, cur, i);
+      // (the wait-ring position is read beside the message body, not behind the branches on it)
+      const uint32_t wn_i = __shfl_sync(FULL, wn, i), wh_i = __shfl_sync(FULL, wh, i);
       const uint32_t slot = (uint32_t)(body & 0xFFFFu), flags = (uint32_t)(body >> 16) & 0xFFu;
       if (TRACE) trace(TR_RECV_DONE, i, rJ[slot], flags);
       uint32_t out = 0;
@@ -421,8 +423,10 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
           const unsigned long long prod = (unsigned long long)n_in * R.out_num;
           const unsigned long long o64 =
               R.out_fixed + (R.out_den == 1 ? prod
-                                            : (prod < 0xFFFFFFFFull ? (unsigned long long)((uint32_t)prod / R.out_den)
-                                                                    : prod / R.out_den));
+                             : (prod < 0xFFFFFFFFull ? (unsigned long long)(R.out_den < 256u
+                                                                                ? div_rcp((uint32_t)prod, R.out_den, P.rcp_fn[R.out_den])
+                                                                                : (uint32_t)prod / R.out_den)
+                                                     : prod / R.out_den));
           out = o64 > 65535ull ? 65535u : (uint32_t)o64;
         }
       }
@@ -432,7 +436,6 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
       }
       if (!(flags & F_CLOSES)) return;
       if (out > 0) {
-        const uint32_t wn_i = __shfl_sync(FULL, wn, i);
         if (K1_UNLIKELY(wn_i >= I.wait_cap)) {
           if (TRACE) trace(TR_OVERFLOW, 2, i, 0);
           ovf = true;
@@ -444,7 +447,7 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
           if (lane == (int)i) ++wn1;
         } else {
           const uint32_t pmw = min(I.wait_cap, RS), k = wn_i - (CLS ? __shfl_sync(FULL, wn1, i) : 0u);
-          const uint32_t idx = wrap_add(__shfl_sync(FULL, wh, i), k, pmw);
+          const uint32_t idx = wrap_add(wh_i, k, pmw);
           if (lane == 0) {
             if (!SPILL || k < pmw) at<uint32_t>(Wr, I.off_wait)[idx] = slot | (out << 16);
             else reinterpret_cast<uint32_t*>(gxa(I.gx_wait))[wrap_add(H->gh[2][i], k - RS, I.wait_cap - RS)] =
@@ -502,6 +505,8 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
       const bool e1 = MAXOUT > 1 && act && n_out > 1 && done == (wD & 0xFFFFu);
       const uint32_t m0 = __ballot_sync(FULL, e0);
       const uint32_t m1 = MAXOUT > 1 ? __ballot_sync(FULL, e1) : 0u;
+      // (issued beside the emission votes: the emissions below change neither done nor out)
+      const uint32_t fin = __ballot_sync(FULL, act && done == out);
       uint32_t wC = 0, wE = 0;
       if (m0 | m1) {
         wC = bat[64 + lane];
@@ -627,7 +632,6 @@ k1_simulate(const uint8_t* __restrict__ blob, Work* __restrict__ work, uint8_t* 
         if (act && done == 1u) atomicCAS(&rFF[slot], kUnsetFF, t - rA[slot]);
         __syncwarp();
       }
-      const uint32_t fin = __ballot_sync(FULL, act && done == out);
       if (!fin) {  // common case: write the advanced words back in place (stale slots included)
         bat[32 + lane] = wB;
         if (m0 | m1) {
