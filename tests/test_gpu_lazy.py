@@ -1,4 +1,5 @@
-"""LEAN K1's lazy deliveries, emit-ahead source runs, RECV chains and advance first feedback
+"""LEAN K1's lazy deliveries, emit-ahead source runs, RECV chains, advance first feedback and
+chained resume (§5.8: full batches with waiting items, window closes and B changes inside chunk RECVs)
 against the oracle and against the
 generic kernel (which delivers every message as its own event and ends every run at an emission point):
 P2-X / P2-SPEC variants that exercise every branch -- TOKEN / FUNCTION / BATCH, deep batches (B = 32) whose
@@ -34,7 +35,8 @@ CANDS = [W.static("token"), W.static("function"), W.static("batch"), W.adaptive(
 
 
 @pytest.mark.parametrize("variant", ["base", "b32_room", "tiny_flight", "slow_net", "small_inbox", "det_boundary",
-                                     "spec_chunk1", "series", "slow_recv", "fast_recv", "tiny_inbox"])
+                                     "spec_chunk1", "series", "slow_recv", "fast_recv", "tiny_inbox",
+                                     "chain_full_batch", "chain_window_b"])
 def test_lazy_and_ahead_variants(variant):
     p = W.p2_x()
     g = W.grid(copy.deepcopy(CANDS), [W.poisson(m) for m in (3994000, 998500, 469882, 347304)], n_seeds=3,
@@ -60,6 +62,16 @@ def test_lazy_and_ahead_variants(variant):
     elif variant == "tiny_inbox":      # hard messages queue behind chains into a 3-slot inbox: overflow ticks
         p["roles"][1]["inbox_cap"] = 3
         p["roles"][1]["cost"]["h"] = 30000
+    elif variant == "chain_full_batch":   # chained resume with a full batch and items waiting
+        p["roles"][1]["max_num_seqs"] = 1
+        p["roles"][1]["cost"].update(h=3000, beta=10)
+        p["window"] = 37_000              # window closes (possible B changes) inside many chunk RECVs
+    elif variant == "chain_window_b":     # SLO batch control on the tester: B changes at window closes
+        p["roles"][1]["max_num_seqs"] = 2
+        p["window"] = 53_000
+        g["candidates"] = g["candidates"] + [
+            W.adaptive(["token"], batch_roles=[1], q_hi=1, policy_slo=2_000_000, dwell=1),
+            W.adaptive(["token"], lo=100, hi=200, batch_roles=[1], q_hi=3, policy_slo=800_000, dwell=1)]
     elif variant == "series":
         g["series_stride"], g["series_slots"], g["series_windows"] = 7, 9, 200
         series = True
