@@ -99,3 +99,30 @@ def make_case(seed):
                max_ticks=int(r.choice([0, 0, 0, 40_000_000])))
     obj = str(r.choice(OBJECTIVES[:6] + (["p99_e2e_int"] if cls else [])))
     return p, g, obj
+
+
+def make_lean_case(seed):
+    """make_case(seed) with the level-0 / level-1 features stripped (KV, classes, pacing, LOAD metric,
+    truncation, extra instances, fan-out, route overrides, stale JSQ), so it runs on the LEAN K1 and its
+    shortcuts (lazy deliveries, silent RECVs, emit-ahead, chained resume) while keeping
+    the random costs, capacities, modes, controllers and arrivals."""
+    p, g, obj = make_case(seed)
+    p.pop("kv", None)
+    for r in p["roles"]:
+        r["n_instances"] = 1
+        r["route"] = "jsq"
+        r["inst_cost"] = None
+    for k, l in enumerate(p["links"]):
+        l["src"], l["dst"], l["pacing_gap"] = k, k + 1, 0
+    for a in g["arrivals"]:
+        for x in a:
+            x.pop("interactive", None)
+    for c in g["candidates"]:
+        for key in ("prio", "admit", "admit_band", "kv", "pacing_gap", "stale_jsq"):
+            c.pop(key, None)
+        c["route"] = None
+        if c.get("metric") == "load":
+            c["metric"] = "busy"
+        c["select_role"] = None
+    g["max_ticks"] = 0
+    return p, g, ("p99_e2e" if obj == "p99_e2e_int" else obj)
