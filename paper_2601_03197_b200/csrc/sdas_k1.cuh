@@ -16,7 +16,9 @@
 // admission gate, per-class metrics.  Pipelines without interactive requests never pay for it.
 // LV: 0 generic; 1 = no KV / pacing / classes / LOAD metric / truncation (compiled out);
 // 2 (LEAN) = level 1 + one instance per role and no fan-out: routing is the identity.  Shrinks the
-// I-cache-bound hot loop.
+// I-cache-bound hot loop.  LEAN also skips events that change nothing observable: deliveries into busy
+// instances, emission points of the source's runs, silent RECVs and the ends of RECVs that a held batch's
+// run follows -- bit-identical to event-per-step execution.
 
 #define K1_UNLIKELY(x) (x)   // marks cold branches (__builtin_expect layout measured +2 % slower)
 
